@@ -1,0 +1,566 @@
+"""Pins of the fp64 oracle against what the paper and mathematics fix.
+
+Every test here checks the oracle against something other than itself:
+values printed in the paper (tests/golden/), closed forms, invariants,
+special cases reducing to textbook results, or brute force.  CPU only.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from oracle import OracleSim, dsm, elastica
+from conftest import read_golden_kv, read_golden_table
+
+KV = read_golden_kv("worked_examples.txt")
+L = 1e-3
+
+
+def mat(E=1e6, nu=0.35, rho=1000.0, cte=0.0, mu_s=0.0, mu_d=0.0):
+    return dict(E=E, nu=nu, rho=rho, cte=cte, mu_s=mu_s, mu_d=mu_d)
+
+
+def sim(cells, mats, **env):
+    e = W._env(**env)
+    cells = np.asarray(cells, np.uint8)
+    s = W.Scene("pin", cells, L, mats, e)
+    o = OracleSim(cells, L, mats, e)
+    o.set_state(*s.initial_state())
+    return o, s
+
+
+# --------------------------------------------------------------- Eq. 1-12
+def test_composite_worked_examples():
+    Ec, Gc, muc = oracle.composite(1e6, 0.3, 3e6, 0.3)
+    assert Ec == pytest.approx(KV["composite_E_1MPa_3MPa"], rel=1e-12)
+    Ec, _, _ = oracle.composite(1e6, 0.3, 100e6, 0.3)
+    assert Ec == pytest.approx(KV["composite_E_1MPa_100MPa"], rel=1e-3)
+    # identical constituents: E_c = E and mu_c recovers nu
+    Ec, Gc, muc = oracle.composite(2.5e6, 0.41, 2.5e6, 0.41)
+    assert Ec == pytest.approx(2.5e6, rel=1e-15) and muc == pytest.approx(0.41, abs=1e-14)
+    # symmetric and bounded by the constituents
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        E1, E2 = 10 ** rng.uniform(4, 9, 2)
+        n1, n2 = rng.uniform(-0.5, 0.49, 2)
+        a = oracle.composite(E1, n1, E2, n2)
+        b = oracle.composite(E2, n2, E1, n1)
+        assert a == b
+        assert min(E1, E2) <= a[0] * (1 + 1e-15) and a[0] <= max(E1, E2) * (1 + 1e-15)
+
+
+def test_beam_constants_worked_examples():
+    G = 1e6 / (2 * 1.3)
+    a1, a2, b1, b2, b3 = oracle.beam_constants(1e6, G, L)
+    assert a1 == pytest.approx(KV["a1_E1MPa_l1mm"], rel=1e-12)
+    assert b1 == pytest.approx(KV["b1_E1MPa_l1mm"], rel=1e-12)
+    assert b2 == pytest.approx(KV["b2_E1MPa_l1mm"], rel=1e-12)
+    assert b3 == pytest.approx(KV["b3_E1MPa_l1mm"], rel=1e-3)
+    assert a2 == pytest.approx(KV["a2_E1MPa_nu0.3_l1mm"], rel=1e-3)
+    # exact ratio identities of Eq. 4, 8-12
+    assert L * b1 == pytest.approx(2 * b2, rel=1e-14)
+    assert L * b2 == pytest.approx(3 * b3, rel=1e-14)
+
+
+# --------------------------------------------------------------- Eq. 6-7, 13-24
+def _golden_K(a1, a2, b1, b2, b3):
+    rows = read_golden_table("eq7_stiffness_matrix.txt")
+    sym = {"a1": a1, "a2": a2, "b1": b1, "b2": b2, "b3": b3, "2b3": 2 * b3, "0": 0.0}
+    K = np.full((12, 12), np.nan)
+    for i, r in enumerate(rows):
+        assert len(r) == 12
+        for j, tok in enumerate(r):
+            if tok == ".":
+                continue
+            neg = tok.startswith("-")
+            v = sym[tok.lstrip("-")]
+            K[i, j] = -v if neg else v
+    for i in range(12):
+        for j in range(12):
+            if np.isnan(K[i, j]):
+                K[i, j] = K[j, i]
+    return K
+
+
+def _quat_small(th):
+    a = np.linalg.norm(th)
+    if a == 0:
+        return np.array([1.0, 0, 0, 0])
+    return np.r_[math.cos(a / 2), math.sin(a / 2) * th / a]
+
+
+def _bond_jacobian(o, axis, h_u=1e-9, h_t=1e-7):
+    e = np.eye(3)[axis]
+    base_a = np.r_[np.zeros(3), 1.0, 0, 0, 0, np.zeros(6)]
+    base_b = np.r_[L * e, 1.0, 0, 0, 0, np.zeros(6)]
+    J = np.zeros((12, 12))
+    for j in range(12):
+        vals = []
+        for sgn in (+1, -1):
+            sa, sb = base_a.copy(), base_b.copy()
+            tgt = sa if j < 6 else sb
+            d = j % 6
+            if d < 3:
+                tgt[d] += sgn * h_u
+            else:
+                th = np.zeros(3); th[d - 3] = sgn * h_t
+                tgt[3:7] = _quat_small(th)
+            Fa, Ma, Fb, Mb = o.bond_loads(0, 0, axis, sa, sb)
+            vals.append(np.r_[Fa, Ma, Fb, Mb])
+        J[:, j] = (vals[0] - vals[1]) / (2 * (h_u if j % 6 < 3 else h_t))
+    return J
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_bond_linearisation_is_minus_eq7(axis):
+    """FD Jacobian of the oracle's bond loads at rest == -[K] of Eq. 7 (rotated
+    to the bond axis by the cyclic permutation, reading R5)."""
+    o, _ = sim(np.ones((1, 1, 2)), [mat(E=1e6, nu=0.3)], zeta_bond=0.0)
+    G = 1e6 / 2.6
+    K = _golden_K(*oracle.beam_constants(1e6, G, L))
+    Pm = np.zeros((3, 3))
+    for r, c in enumerate({0: (0, 1, 2), 1: (1, 2, 0), 2: (2, 0, 1)}[axis]):
+        Pm[r, c] = 1
+    T = np.kron(np.eye(4), Pm)
+    Kw = T.T @ K @ T
+    J = _bond_jacobian(o, axis)
+    scale = np.sqrt(np.outer(np.abs(np.diag(Kw)), np.abs(np.diag(Kw))))
+    assert np.all(np.abs(J + Kw) <= 1e-5 * scale + 1e-12)
+
+
+def test_zero_load_at_rest_and_rigid_motion_nullity():
+    rng = np.random.default_rng(1)
+    cells = rng.integers(0, 3, size=(3, 4, 5)).astype(np.uint8)
+    cells[1, 1, :] = 1
+    mats = [mat(E=1e6, rho=1000), mat(E=3e7, rho=1500, nu=0.2)]
+    o, s = sim(cells, mats, zeta_bond=1.0)
+    pos, quat, P, phi, latch = s.initial_state()
+    # random rigid rotation + translation of the whole body
+    ax = rng.normal(size=3); ax /= np.linalg.norm(ax)
+    q = _quat_small(1.3 * ax)
+    w, x, y, z = q
+    R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                  [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                  [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+    c = pos.mean(0)
+    pos2 = (pos - c) @ R.T + c + np.array([0.01, -0.02, 0.005])
+    quat2 = np.tile(q, (len(pos), 1))
+    # plus a rigid spin about the centroid with a rigid translation velocity
+    omega = np.array([30.0, -10.0, 45.0])
+    vel = np.cross(omega, pos2 - c) + np.array([0.3, 0.1, -0.2])
+    rho = np.array([m["rho"] for m in mats])[cells.ravel()[cells.ravel() > 0] - 1]
+    m = rho * L ** 3
+    P2 = m[:, None] * vel
+    phi2 = (m * L * L / 6)[:, None] * omega[None, :]
+    o.set_state(pos2, quat2, P2, phi2, latch)
+    o.step(1)
+    st = o.read_state()
+    dP = st.linmom - P2
+    dphi = st.angmom - phi2
+    # load scale: one bond at 1% strain
+    fscale = 1e6 * L * 1e-2 * o.dt
+    assert np.abs(dP).max() <= 1e-12 * fscale
+    assert np.abs(dphi).max() <= 1e-12 * fscale * L
+
+
+def test_newton3_per_bond_and_moment_balance():
+    o, _ = sim(np.ones((1, 1, 2)), [mat(), mat(E=2e7, rho=1300)], zeta_bond=1.0)
+    o0, _ = sim(np.ones((1, 1, 2)), [mat(), mat(E=2e7, rho=1300)], zeta_bond=0.0)
+    rng = np.random.default_rng(2)
+    for axis in range(3):
+        for _ in range(30):
+            e = np.eye(3)[axis]
+            du = rng.normal(size=(2, 3))
+            dth = rng.normal(size=(2, 3))
+            mom = rng.normal(size=(4, 3))
+            res = []
+            for eps in (1e-3, 1e-4):
+                sa = np.r_[eps * L * du[0], _quat_small(eps * dth[0]), 1e-9 * mom[0],
+                           1e-15 * mom[1]]
+                sb = np.r_[L * e + eps * L * du[1], _quat_small(eps * dth[1]),
+                           1e-9 * mom[2], 1e-15 * mom[3]]
+                Fa, Ma, Fb, Mb = o.bond_loads(0, 1, axis, sa, sb)
+                assert np.array_equal(Fb, -Fa)
+                # elastic moment balance about voxel a holds to O(strain^2) (SURVEY
+                # 8c #18); the bond damping force of Eq. 34 is not collinear with r,
+                # so balance is checked on the undamped loads.
+                Fa, Ma, Fb, Mb = o0.bond_loads(0, 1, axis, sa, sb)
+                r = sb[:3] - sa[:3]
+                res.append(np.linalg.norm(Ma + Mb + np.cross(r, Fb)))
+            assert 70 <= res[0] / res[1] <= 130
+
+
+# --------------------------------------------------------------- Table 1
+def _cantilever(dims, force, zeta_ground, E=1e6):
+    nx, ny, nz = dims
+    cells = np.ones((nz, ny, nx), np.uint8)
+    o, s = sim(cells, [mat(E=E)], zeta_bond=1.0, zeta_ground=zeta_ground)
+    ijk = s.voxel_coords()
+    fixed = (ijk[:, 0] == 0).astype(np.uint8)
+    fext = np.zeros((len(ijk), 3))
+    end = ijk[:, 0] == nx - 1
+    fext[end, 2] = -force / end.sum()
+    o.set_boundary(fixed, fext)
+    return o, s, fixed.astype(bool), fext
+
+
+def _table1():
+    return {r[0]: dict(dims=tuple(int(x) for x in r[1:4]), F=float(r[4]), ms=float(r[5]),
+                       dsm=float(r[6]), an=float(r[7])) for r in read_golden_table("table1.txt")}
+
+
+@pytest.mark.parametrize("geom,tol", [("thin", 0.005), ("thick", 0.01)])
+def test_table1_direct_stiffness(geom, tol):
+    t = _table1()[geom]
+    nx, ny, nz = t["dims"]
+    o, s, fixed, fext = _cantilever(t["dims"], t["F"], 0.0)
+    u = dsm.solve(s.cells, L, s.materials, fixed, fext)
+    assert np.abs(u[:, 2]).max() * 1e3 == pytest.approx(t["dsm"], rel=tol)
+    if geom == "thin":   # P L^3 / 3EI with span (N-1) l
+        an = elastica.linear_tip_deflection(t["F"], (nx - 1) * L, 1e6, L ** 4 / 12)
+        assert an * 1e3 == pytest.approx(t["an"], rel=tol)
+
+
+def test_dsm_free_cube_has_six_rigid_modes():
+    K, _ = dsm.assemble(np.ones((3, 3, 3), np.uint8), L, [mat()])
+    ev = np.linalg.eigvalsh(K.toarray())
+    assert np.all(ev > -1e-9 * ev.max())
+    assert int(np.sum(np.abs(ev) < 1e-9 * ev.max())) == 6
+
+
+def test_table1_dynamic_relaxation_thin():
+    t = _table1()["thin"]
+    o, s, _, _ = _cantilever(t["dims"], t["F"], 0.003)
+    p0 = o.read_state().pos.copy()
+    o.step(60000)
+    d = np.abs(o.read_state().pos - p0)[:, 2].max() * 1e3
+    assert 0.81 <= d <= 0.83                                  # paper: 0.822
+    assert d == pytest.approx(t["ms"], rel=2e-3)
+
+
+def test_table1_dynamic_relaxation_thick():
+    t = _table1()["thick"]
+    o, s, fixed, fext = _cantilever(t["dims"], t["F"], 0.013)
+    p0 = o.read_state().pos.copy()
+    o.step(12000)
+    d = np.abs(o.read_state().pos - p0)[:, 2].max() * 1e3
+    # paper 0.538 (mass/spring).  Our literal P:189 frame (voxel a's frame)
+    # softens by +0.9% over the DSM at this load instead of the paper's -1.5%;
+    # DESIGN.md §3 "known discrepancy".  Pinned at 3% of the printed value.
+    assert d == pytest.approx(t["ms"], rel=0.03)
+
+
+def test_relaxation_linear_limit_equals_dsm():
+    """Small load: dynamic relaxation -> the linear DSM solution exactly."""
+    o, s, fixed, fext = _cantilever((10, 5, 5), 1e-4, 0.013)
+    p0 = o.read_state().pos.copy()
+    o.step(12000)
+    ud = o.read_state().pos - p0
+    u = dsm.solve(s.cells, L, s.materials, fixed, fext)
+    assert np.abs(ud - u[:, :3]).max() <= 1e-4 * np.abs(u[:, :3]).max()
+
+
+def test_cantilever_linear_regime_pl3_3ei():
+    o, s, _, _ = _cantilever((10, 1, 1), 1e-5, 0.013)
+    p0 = o.read_state().pos.copy()
+    o.step(20000)
+    d = (p0 - o.read_state().pos)[-1, 2]
+    an = elastica.linear_tip_deflection(1e-5, 9 * L, 1e6, L ** 4 / 12)
+    assert an == pytest.approx(29.16e-6, rel=1e-12)
+    assert d == pytest.approx(an, rel=5e-3)
+
+
+def test_c1_as_written_matches_elastica():
+    sc = W.cantilever()
+    o = OracleSim(sc.cells, sc.lattice_dim, sc.materials, sc.env, sc.origin)
+    o.set_boundary(sc.fixed, sc.fext)
+    o.set_state(*sc.initial_state())
+    p0 = o.read_state().pos.copy()
+    o.step(sc.steps)
+    d = (p0 - o.read_state().pos)[-1, 2]
+    el, _ = elastica.tip_deflection(1e-3, 9 * L, 1e6, L ** 4 / 12)
+    assert el == pytest.approx(2.652e-3, rel=1e-3)
+    assert d == pytest.approx(el, rel=0.02)
+
+
+# --------------------------------------------------------------- Eq. 27-32
+def test_dt_worked_example_and_scaling():
+    o, _ = sim(np.ones((1, 1, 2)), [mat(E=1e6, rho=1000)])
+    assert o.dt == pytest.approx(KV["dt_k1000_m1e-6"], rel=1e-3)
+    assert o.dt == pytest.approx(1 / (2 * math.pi * math.sqrt(1000 / 1e-6)), rel=1e-14)
+    o2, _ = sim(np.ones((1, 1, 2)), [mat(E=1e8, rho=1000)])
+    assert o2.dt == pytest.approx(o.dt / 10, rel=1e-13)
+
+
+def test_free_fall_semi_implicit_closed_form():
+    o, s = sim(np.ones((1, 1, 1)), [mat()], gravity=9.81)
+    z0 = o.read_state().pos[0, 2]
+    dt, m = o.dt, 1e-6
+    for n in (1, 10, 1000):
+        o2, _ = sim(np.ones((1, 1, 1)), [mat()], gravity=9.81)
+        o2.step(n)
+        st = o2.read_state()
+        assert st.linmom[0, 2] / m == pytest.approx(-9.81 * n * dt, rel=1e-12)
+        assert st.pos[0, 2] == pytest.approx(z0 - 9.81 * dt * dt * n * (n + 1) / 2, rel=1e-13)
+
+
+def test_two_voxel_axial_oscillator_discrete_frequency():
+    o, s = sim(np.ones((1, 1, 2)), [mat()], zeta_bond=0.0)
+    pos, quat, P, phi, latch = s.initial_state()
+    pos[1, 0] += 1e-9
+    o.set_state(pos, quat, P, phi, latch)
+    xs = []
+    for _ in range(400):
+        xs.append(o.read_state().pos[1, 0] - o.read_state().pos[0, 0] - L)
+        o.step(1)
+    x = np.array(xs)
+    # exact recurrence of the linear symplectic-Euler oscillator
+    c = np.dot(x[2:] + x[:-2], x[1:-1]) / (2 * np.dot(x[1:-1], x[1:-1]))
+    w2 = 2 * 1000.0 / 1e-6
+    assert c == pytest.approx(1 - w2 * o.dt ** 2 / 2, abs=1e-6)
+
+
+def test_linear_momentum_conserved_free_body():
+    rng = np.random.default_rng(3)
+    cells = rng.integers(1, 3, size=(3, 3, 4)).astype(np.uint8)
+    o, s = sim(cells, [mat(), mat(E=1e7, rho=1400)], zeta_bond=1.0)
+    pos, quat, P, phi, latch = s.initial_state()
+    pos += rng.normal(size=pos.shape) * 2e-6
+    P += rng.normal(size=P.shape) * 1e-9
+    o.set_state(pos, quat, P, phi, latch)
+    P0 = o.read_state().linmom.sum(0)
+    o.step(10000)
+    st = o.read_state()
+    scale = np.abs(st.linmom).sum() + np.abs(P).sum()
+    assert np.abs(st.linmom.sum(0) - P0).max() <= 1e-12 * scale
+
+
+def _angmom(st):
+    return (np.cross(st.pos, st.linmom) + st.angmom).sum(0)
+
+
+def test_angular_momentum_drift_scales_with_amplitude_squared():
+    rng = np.random.default_rng(4)
+    cells = np.ones((2, 3, 4), np.uint8)
+    drift = []
+    dirs = rng.normal(size=(24, 3))
+    for eps in (1e-5, 1e-6):
+        o, s = sim(cells, [mat()], zeta_bond=0.0)
+        pos, quat, P, phi, latch = s.initial_state()
+        pos = pos + eps * L * dirs / 1e-3 * 1e-3
+        o.set_state(pos, quat, P, phi, latch)
+        L0 = _angmom(o.read_state())
+        Lmax = 0.0
+        for _ in range(20):
+            o.step(100)
+            Lmax = max(Lmax, np.linalg.norm(_angmom(o.read_state()) - L0))
+        drift.append(Lmax)
+    ratio = drift[0] / drift[1]
+    assert 50 <= ratio <= 200, ratio
+
+
+# --------------------------------------------------------------- Eq. 39-40
+def test_thermal_free_expansion_factor():
+    assert 1 + 0.02 * 30 == pytest.approx(KV["thermal_factor_a0.02_dT30"])
+    cells = np.ones((3, 3, 3), np.uint8)
+    o, s = sim(cells, [mat(cte=0.02)], zeta_bond=1.0, zeta_ground=0.05,
+               T_amp=30.0, T_freq=0.0, T_phase=math.pi / 2)
+    o.step(20000)
+    st = o.read_state()
+    ijk = s.voxel_coords()
+    idx = {tuple(c): n for n, c in enumerate(ijk)}
+    lens = []
+    for (i, j, k), a in idx.items():
+        for d in range(3):
+            nb = [i, j, k]; nb[d] += 1
+            b = idx.get(tuple(nb))
+            if b is not None:
+                lens.append(np.linalg.norm(st.pos[b] - st.pos[a]))
+    assert np.allclose(np.array(lens) / L, 1.6, rtol=1e-3)
+
+
+def test_thermal_nonpositive_rest_length_is_a_fault():
+    o, _ = sim(np.ones((1, 1, 2)), [mat(cte=0.02)], T_amp=60.0, T_phase=-math.pi / 2)
+    with pytest.raises(FloatingPointError):
+        o.step(1)
+
+
+# --------------------------------------------------------------- floor & friction
+def test_floor_resting_penetration():
+    o, s = sim(np.ones((1, 1, 1)), [mat(mu_s=0.5, mu_d=0.5)], gravity=9.81, floor_on=1,
+               zeta_col=1.0)
+    o.step(5000)
+    st = o.read_state()
+    pen = 0.5 * L - st.pos[0, 2]
+    assert pen == pytest.approx(1e-6 * 9.81 / (1e6 * L), rel=1e-6)
+
+
+def _floor_voxel(mu_s, mu_d, pen, vx):
+    o, s = sim(np.ones((1, 1, 1)), [mat(mu_s=mu_s, mu_d=mu_d)], floor_on=1)
+    m = 1e-6
+    o.set_state(np.array([[0.0, 0.0, 0.5 * L - pen]]), np.array([[1.0, 0, 0, 0]]),
+                np.array([[m * vx, 0.0, 0.0]]), np.zeros((1, 3)), np.zeros(1, np.uint8))
+    return o
+
+
+def test_friction_eq38_halting_threshold():
+    # Eq. 38 example structure: halt iff V_l <= mu_d F_n dt / m.
+    pen, mu_d, m = 1e-6, 0.5, 1e-6
+    Fn = 1e6 * L * pen
+    o = _floor_voxel(mu_d, mu_d, pen, 0.0)
+    thr = mu_d * Fn * o.dt / m
+    o = _floor_voxel(mu_d, mu_d, pen, 0.999 * thr)
+    o.step(1)
+    st = o.read_state()
+    assert st.linmom[0, 0] == 0.0 and st.latch[0] == 1
+    o = _floor_voxel(mu_d, mu_d, pen, 1.001 * thr)
+    o.step(1)
+    st = o.read_state()
+    assert st.latch[0] == 0
+    assert st.linmom[0, 0] == pytest.approx(m * 1.001 * thr - mu_d * Fn * o.dt, rel=1e-9)
+
+
+def test_friction_block_ramp_stick_slip_and_halt():
+    """AC8: stays until |F_l| > mu_s F_n (+-1 step), decelerates at
+    mu_d g, halts without crossing zero."""
+    mu_s, mu_d, g, m = 0.6, 0.4, 9.81, 1e-6
+    o, s = sim(np.ones((1, 1, 1)), [mat(mu_s=mu_s, mu_d=mu_d)], gravity=g, floor_on=1,
+               zeta_col=1.0)
+    o.step(3000)                          # settle vertically, latched
+    assert o.read_state().latch[0] == 1
+    rate = mu_s * m * g / 500.0           # breakaway expected at ~500 steps
+    moved_at = None
+    for n in range(1, 800):
+        o.set_boundary(None, np.array([[rate * n, 0.0, 0.0]]))
+        o.step(1)
+        if o.read_state().linmom[0, 0] != 0.0:
+            moved_at = n
+            break
+    assert moved_at is not None and abs(moved_at - 500) <= 1
+    o.set_boundary(None, np.array([[rate * (moved_at + 200), 0.0, 0.0]]))
+    o.step(200)                           # slide
+    o.set_boundary(None, None)            # release: decelerate under friction
+    v = []
+    for _ in range(2000):
+        o.step(1)
+        v.append(o.read_state().linmom[0, 0] / m)
+    v = np.array(v)
+    moving = np.nonzero(v > 0)[0]
+    assert len(moving) > 20 and np.all(v >= 0)
+    decel = -(v[moving[-1]] - v[moving[0]]) / ((moving[-1] - moving[0]) * o.dt)
+    assert decel == pytest.approx(mu_d * g, rel=0.02)
+    assert v[-1] == 0.0 and o.read_state().latch[0] == 1
+
+
+# --------------------------------------------------------------- self collision
+def test_contact_penalty_law_and_momentum():
+    cells = np.zeros((1, 1, 6), np.uint8); cells[0, 0, 0] = 1; cells[0, 0, 5] = 1
+    o, s = sim(cells, [mat()], self_collision=1, zeta_col=0.0)
+    pos, quat, P, phi, latch = s.initial_state()
+    pos[1] = pos[0] + np.array([0.9 * L, 0, 0])      # overlap q = 0.1 l
+    o.set_state(pos, quat, P, phi, latch)
+    assert o.contact_pairs().tolist() == [[0, 1]]
+    o.step(1)
+    st = o.read_state()
+    F = st.linmom / o.dt
+    assert F[0] == pytest.approx([-1e6 * L * 0.1 * L, 0, 0], rel=1e-9)
+    assert np.array_equal(st.linmom[0], -st.linmom[1])
+
+
+def test_contact_excludes_lattice_neighbours_within_manhattan_3():
+    # a 1x1x4 rod: ends are Manhattan 3 apart -> never a contact pair
+    o, s = sim(np.ones((1, 1, 4)), [mat()], self_collision=1)
+    pos, quat, P, phi, latch = s.initial_state()
+    pos[3] = pos[0] + np.array([0.5 * L, 0, 0])
+    o.set_state(pos, quat, P, phi, latch)
+    assert len(o.contact_pairs()) == 0
+
+
+def test_contact_pairs_brute_force_definition():
+    rng = np.random.default_rng(5)
+    cells = (rng.random((4, 4, 6)) < 0.6).astype(np.uint8)
+    o, s = sim(cells, [mat()], self_collision=1)
+    pos, quat, P, phi, latch = s.initial_state()
+    pos = pos + rng.normal(size=pos.shape) * 0.4 * L
+    o.set_state(pos, quat, P, phi, latch)
+    ijk = s.voxel_coords()
+    N = len(ijk)
+    cnt = np.zeros(N, int)
+    idx = {tuple(c): n for n, c in enumerate(ijk)}
+    for n, (i, j, k) in enumerate(ijk):
+        for d in ((1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)):
+            cnt[n] += (i + d[0], j + d[1], k + d[2]) in idx
+    surf = np.nonzero(cnt < 6)[0]
+    expect = []
+    for x in range(len(surf)):
+        for y in range(x + 1, len(surf)):
+            a, b = surf[x], surf[y]
+            if np.abs(ijk[a] - ijk[b]).sum() <= 3:
+                continue
+            if np.linalg.norm(pos[a] - pos[b]) < L:
+                expect.append([a, b])
+    got = o.contact_pairs().tolist()
+    assert got == expect and len(expect) > 0
+
+
+# --------------------------------------------------------------- topology, regions
+def test_topology_counts():
+    o, _ = sim(np.ones((3, 3, 3)), [mat()])
+    assert o.num_bonds == KV["cube3_bonds"] and o.num_surface == KV["cube3_surface"]
+    o, _ = sim(np.ones((1, 1, 1)), [mat()])
+    assert o.num_bonds == 0 and o.num_surface == 1
+    o, _ = sim(np.ones((1, 1, 2)), [mat()])
+    assert o.num_bonds == 1
+
+
+def test_app_a_regions():
+    sc = W.app_a_beam()
+    o = OracleSim(sc.cells, sc.lattice_dim, sc.materials, sc.env)
+    for kind, org, size, force in sc.extra["regions"]:
+        o.add_region(kind, org, size, force)
+    pos, quat, P, phi, latch = sc.initial_state()
+    ijk = sc.voxel_coords()
+    o.set_state(pos, quat, P, phi, latch)
+    o.step(1)
+    st = o.read_state()
+    Fz = st.linmom[:, 2] / o.dt
+    forced = ijk[:, 1] == 9
+    assert forced.sum() == 25
+    assert np.allclose(Fz[forced], KV["appA_force_per_voxel_N"], rtol=1e-12)
+    assert np.abs(Fz[~forced]).max() <= 1e-12   # rounding of the rest geometry
+    # fixed: never integrated
+    sc2 = W.app_a_beam()
+    o = OracleSim(sc2.cells, sc2.lattice_dim, sc2.materials, sc2.env)
+    o.add_region(*sc2.extra["regions"][0])
+    P = np.tile([1e-6 * 1.0, 0, 0], (len(pos), 1))
+    o.set_state(pos, quat, P, phi, latch)
+    o.step(1)
+    st = o.read_state()
+    fixed = np.all(st.pos == pos, axis=1)
+    assert fixed.sum() == KV["appA_fixed_voxels"] and np.all(ijk[fixed, 1] == 0)
+
+
+# --------------------------------------------------------------- determinism, faults
+def test_determinism_reruns_and_thread_counts():
+    sc = W.cube(contact_variant=True, n=6)
+    outs = []
+    for threads in (1, 4, 1):
+        o = OracleSim(sc.cells, sc.lattice_dim, sc.materials, sc.env, sc.origin)
+        o.set_threads(threads)
+        o.set_state(*sc.initial_state())
+        o.step(150)
+        st = o.read_state()
+        outs.append(np.concatenate([st.pos.ravel(), st.quat.ravel(), st.linmom.ravel(),
+                                    st.angmom.ravel()]))
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_divergence_names_voxel_and_step():
+    o, s = sim(np.ones((1, 1, 3)), [mat()])
+    pos, quat, P, phi, latch = s.initial_state()
+    P[2, 1] = np.nan
+    o.set_state(pos, quat, P, phi, latch)
+    with pytest.raises(FloatingPointError, match="voxel 1 at step 0"):
+        o.step(5)
