@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark of the voxel stepper (arXiv:1212.2845) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one rank per GPU, NCCL); the lattice is split
+into x-slabs and each rank steps its slab, exchanging ghost planes by NCCL
+send/recv inside libvoxsim.so.  One step = one full pass of the hot path
+(clock, bond kernel K3, gather-integrate kernel K4) over the whole lattice.
+
+Rank 0 prints ONE JSON line.  ``value`` is whole-job voxel-steps/s with the
+state resident in HBM (CUDA events on the library stream, max over ranks);
+``e2e`` is the same metric through the public API with the state uploaded
+from pinned host memory and read back every episode; ``roofline`` is the
+dominant kernel's algorithmic HBM bytes per launch over its live average
+launch duration; ``cpu_baseline`` is the fp64 oracle (test infrastructure) on
+a bounded sample, timed on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "voxel-steps/sec and achieved HBM GB/s vs peak"
+UNIT = "voxel-steps/s"
+
+# Algorithmic HBM bytes per voxel-step, fp32 / fp64
+ALG_BYTES = {
+    32: {"bonds": 56 + 108, "integrate": 108 + 56 + 56},
+    64: {"bonds": 112 + 216, "integrate": 216 + 112 + 112},
+}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def scene_for(name, precision):
+    if name == "C5":
+        return W.block(precision=precision)
+    sc = W.get(name)
+    sc.precision = precision
+    return sc
+
+
+# ------------------------------------------------------------------ reference arm
+def oracle_sample(cfg, precision, budget_s=10.0):
+    """The fp64 oracle on a bounded sample of the workload: (voxel-steps/s,
+    sample description, threads, total voxel-steps)."""
+    from oracle import OracleSim
+    if cfg == "C5":
+        sc = W.block(16, 256, 256, precision=precision)   # first 16 x-planes of C5
+        desc = "C5 sub-slab 16x256x256 (1,048,576 voxels, same recipe)"
+    else:
+        sc = scene_for(cfg, precision)
+        desc = f"{sc.name} full lattice"
+    o = OracleSim(sc.cells, sc.lattice_dim, sc.materials, sc.env, sc.origin)
+    threads = os.cpu_count() or 1
+    o.set_threads(threads)
+    if sc.fixed is not None or sc.fext is not None:
+        o.set_boundary(sc.fixed, sc.fext)
+    o.set_state(*sc.initial_state())
+    o.step(1)
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        o.step(1)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or steps >= 100000:
+            break
+    rate = o.n * steps / el
+    return rate, f"{desc}, {steps} steps in {el:.1f} s", threads, o.n * steps
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    if args.config == "C5":
+        sc = W.block(16, 256, 256, precision=args.precision)
+        desc = "C5 sub-slab 16x256x256 (1,048,576 voxels, same recipe)"
+    else:
+        sc = scene_for(args.config, args.precision)
+        desc = f"{sc.name} full lattice"
+    from oracle import OracleSim as O
+    o = O(sc.cells, sc.lattice_dim, sc.materials, sc.env, sc.origin)
+    threads = os.cpu_count() or 1
+    o.set_threads(threads)
+    if sc.fixed is not None or sc.fext is not None:
+        o.set_boundary(sc.fixed, sc.fext)
+    o.set_state(*sc.initial_state())
+    for _ in range(args.warmup):
+        o.step(1)
+    t0 = time.perf_counter()
+    o.step(args.steps)
+    el = time.perf_counter() - t0
+    val = o.n * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (oracle sample: {desc})"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"{desc}, {args.steps} timed steps"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1212_2845_b200 import from_scene, nccl_unique_id
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            print("use torchrun for --gpus > 1", file=sys.stderr)
+            return 2
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nid = None
+    if world > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+
+    sc = scene_for(args.config, args.precision)
+    lat = from_scene(sc, precision=args.precision, device=local, rank=rank, nranks=world,
+                     nccl_id=nid, init_state=sc.v0 is not None)
+    N = lat.num_voxels
+    stream = torch.cuda.ExternalStream(lat.stream, device=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    # warm-up (graphs captured / tables uploaded)
+    lat.step(max(args.warmup, 3))
+    barrier()
+
+    # ---- timed region: K steps, state resident in HBM
+    lat.set_instrumentation(True)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    lat.step(args.steps)
+    ev1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    kt = lat.kernel_times()
+    lat.set_instrumentation(False)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = N * args.steps / (ms_max / 1e3)
+
+    # ---- roofline of the dominant kernel (live CUDA-event durations)
+    x0, x1 = lat.owned_planes()
+    vox_rank = N * (x1 - x0) / sc.cells.shape[2]   # dense boxes: voxels per rank
+    alg = ALG_BYTES[args.precision]
+    avg = {k: kt[k][0] / max(kt[k][1], 1) for k in ("bonds", "integrate")}
+    # bonds is launched once per step at N=1 (3x with the halo split)
+    per_step_ms = {k: kt[k][0] / args.steps for k in ("bonds", "integrate")}
+    dom = max(per_step_ms, key=per_step_ms.get)
+    peak, peak_src = _peaks()
+    achieved = alg[dom] * vox_rank / (per_step_ms[dom] / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            tr = json.load(open(tp))
+            key = f"{args.config}:fp{args.precision}:{dom}"
+            traffic = tr.get(key)
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": "k_bonds (K3)" if dom == "bonds" else "k_integrate (K4)",
+            "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "alg_bytes_per_voxel": alg[dom],
+            "avg_launch_ms": avg[dom],
+            "kernels": {k: {"ms_per_step": per_step_ms[k],
+                            "GBps": alg[k] * vox_rank / (per_step_ms[k] / 1e3) / 1e9}
+                        for k in ("bonds", "integrate")},
+            "step_GBps_alg": (alg["bonds"] + alg["integrate"]) * N
+            / (ms_max / args.steps / 1e3) / 1e9}
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        st0 = sc.initial_state()
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa
+        hin = [pin(a) for a in st0]
+        from paper_1212_2845_b200 import State
+        hout = State(*[pin(np.empty_like(a)) for a in st0])
+        K = args.steps
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        tw = time.perf_counter()
+        e0.record(stream)
+        lat.set_state(*hin)
+        lat.set_step(0)
+        lat.step(K)
+        lat.read_state(hout)
+        e1.record(stream)
+        barrier()
+        tw = time.perf_counter() - tw
+        ems = e0.elapsed_time(e1)
+        t = torch.tensor([ems, tw * 1e3], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t[1].item())   # host wall clock bounds the device timeline
+        bi = sum(a.nbytes for a in hin)
+        bo = sum(a.nbytes for a in (hout.pos, hout.quat, hout.linmom, hout.angmom, hout.latch))
+        e2e = {"value": N * K / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": bi / K, "d2h_bytes_per_step": bo / K,
+               "episode": f"set_state (H2D) + {K} steps + read_state (D2H) per episode; "
+                          "bytes per step = episode bytes / K"}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, desc, threads, _ = oracle_sample(args.config, args.precision, args.cpu_budget)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
+            "config": {"workload": f"{sc.name} ({sc.cells.shape[2]}x{sc.cells.shape[1]}x"
+                                   f"{sc.cells.shape[0]}, {N} voxels, {lat.num_bonds} bonds)",
+                       "parallelism": f"x-slab{world}",
+                       "l2": "no flush: working set (state + bond records) >> 126 MB L2"
+                             if N > 1_000_000 else "small lattice, L2-resident"},
+            "clocks": clocks, "gpu_launches": lat.launches_per_step * args.steps * world,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "achieved_GBps_alg": roof["step_GBps_alg"],
+        }
+        print(json.dumps(line), flush=True)
+    lat.destroy()
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--precision", type=int, default=32)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -84,6 +84,7 @@ def lib():
         L.orc_read_state.argtypes = [P, P, P, P, P, P]
         L.orc_set_step.argtypes = [P, ctypes.c_int64]
         L.orc_set_threads.argtypes = [P, ctypes.c_int32]
+        L.orc_set_dt.argtypes = [P, ctypes.c_double]
         L.orc_step.argtypes = [P, ctypes.c_int64]
         L.orc_composite.argtypes = [ctypes.c_double] * 4 + [dp]
         L.orc_beam_constants.argtypes = [ctypes.c_double] * 3 + [dp]
@@ -174,6 +175,9 @@ class OracleSim:
     # --- setup ---
     def set_threads(self, n):
         lib().orc_set_threads(self._h, int(n))
+
+    def set_dt(self, dt):
+        lib().orc_set_dt(self._h, float(dt))
 
     def set_boundary(self, fixed=None, fext=None):
         f = None if fixed is None else np.ascontiguousarray(fixed, dtype=np.uint8)

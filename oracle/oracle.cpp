@@ -480,6 +480,7 @@ int orc_read_state(const orc_sim* s, double* pos, double* quat, double* linmom, 
 int orc_set_step(orc_sim* s, int64_t n) { s->n = n; return 0; }
 int64_t orc_get_step(const orc_sim* s) { return s->n; }
 int orc_set_threads(orc_sim* s, int32_t n) { s->threads = n < 1 ? 1 : n; return 0; }
+int orc_set_dt(orc_sim* s, double dt) { s->dt = dt; return 0; }
 
 void orc_bond_loads(const orc_sim* s, int32_t a_mat, int32_t b_mat, int32_t axis,
                     const double* sa, const double* sb, double dT, double out[12]) {

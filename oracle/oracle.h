@@ -70,6 +70,9 @@ int orc_read_state(const orc_sim* s, double* pos, double* quat, double* linmom,
 int orc_set_step(orc_sim* s, int64_t n);
 int64_t orc_get_step(const orc_sim* s);
 int orc_set_threads(orc_sim* s, int32_t n);
+/* Override the stable step (used when a sub-lattice stands in for a
+ * neighbourhood of a larger lattice whose Eq. 31 dt differs). */
+int orc_set_dt(orc_sim* s, double dt);
 /* Advance n steps.  0 ok, -6 diverged (message names voxel and step). */
 int orc_step(orc_sim* s, int64_t n);
 

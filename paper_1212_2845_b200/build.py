@@ -1,0 +1,65 @@
+"""Build libvoxsim.so (sm_100a) in-tree with nvcc.
+
+    python -m paper_1212_2845_b200.build
+
+Links torch's bundled NCCL (nvidia/nccl, 2.28.x) -- never the system copy --
+so the library and torch.distributed share one NCCL in a process.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libvoxsim.so")
+SOURCES = [os.path.join(HERE, "csrc", "voxsim.cu")]
+DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [
+    os.path.join(ROOT, "include", "voxsim.h")]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dir() -> str:
+    import nvidia  # the torch wheel's CUDA components
+    for p in nvidia.__path__:
+        d = os.path.join(p, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("torch-bundled NCCL (nvidia/nccl) not found")
+
+
+def nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc"):
+        if c and os.path.exists(c):
+            return c
+    return "nvcc"
+
+
+def needs_build() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(p) > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_build():
+        return LIB
+    nd = nccl_dir()
+    tmp = LIB + f".tmp{os.getpid()}"
+    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
+           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
+           "-Xlinker", "-rpath," + os.path.join(nd, "lib"), "-o", tmp, *SOURCES]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,1018 @@
+// voxsim.cu -- host side of the B200 voxel stepper: lattice builder (L1),
+// material tables (Eq. 1-12), step orchestration with CUDA graphs and the
+// NCCL x-slab halo (L3), and the C ABI of include/voxsim.h (L4).
+// Paper: Hiller & Lipson, arXiv:1212.2845.  Readings: DESIGN.md §3.
+#include "voxsim.h"
+#include "vx_kernels.cuh"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+using namespace vx;
+
+namespace {
+
+thread_local std::string g_err;
+
+vx_status fail(vx_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define VX_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(e_ == cudaErrorMemoryAllocation ? VX_ERR_OOM : VX_ERR_CUDA,      \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+
+#define VX_NCCL(call)                                                              \
+  do {                                                                             \
+    ncclResult_t r_ = (call);                                                      \
+    if (r_ != ncclSuccess)                                                         \
+      return fail(VX_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+#define VX_TRY(call)            \
+  do {                          \
+    vx_status s_ = (call);      \
+    if (s_ != VX_OK) return s_; \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  vx_status alloc(size_t b) {
+    if (b == bytes && p) return VX_OK;
+    release();
+    if (b == 0) return VX_OK;
+    VX_CUDA(cudaMalloc(&p, b));
+    bytes = b;
+    return VX_OK;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+const double kPi = 3.14159265358979323846;
+
+}  // namespace
+
+struct vx_lattice {
+  // geometry (global)
+  int nx = 0, ny = 0, nz = 0;
+  double l = 0, origin[3] = {0, 0, 0};
+  int prec = 32;
+  int device = 0, rank = 0, nranks = 1;
+  std::vector<uint8_t> cells;             // x-fastest
+  // slab of this rank
+  int x0 = 0, x1 = 0, xl0 = 0, xl1 = 0;
+  uint32_t nloc = 0, plane = 0;           // plane = ny * nz
+  long long box_base = 0;                 // xl0 * plane
+  long long nbox = 0;                     // nx * plane (global)
+  // counts (global)
+  long long N = 0, nbonds = 0, nsurf = 0;
+  std::vector<long long> box_of_ext;      // global box id of each external voxel
+  std::vector<uint32_t> meta_static;      // local box
+  int max_cell = 0;
+  // boundary (external order)
+  std::vector<uint8_t> fixed;
+  std::vector<double> fext;
+  bool any_ext = false;
+  // materials / env
+  std::vector<vx_material> mats;
+  bool mats_set = false, env_set = false;
+  vx_env env{};
+  double w2max = 0, dt = 0;
+  bool tables_dirty = true;
+  // device
+  cudaStream_t stream = nullptr, comm_stream = nullptr;
+  cudaEvent_t ev_k4 = nullptr, ev_halo = nullptr;
+  DevBuf pos, quat, mom, ang, recA, recB, recC, fextd, cf, mat, pair, clk, meta_d, box_of_ext_d;
+  DevBuf ext_of_local;                    // local box id -> external id (divergence reports)
+  DevBuf pair_w2, mat_w2;
+  // self collision
+  std::vector<int> surf_local;
+  DevBuf surf_d, cellh, bcount, bstart, bitems, rowptr, col;
+  int H = 0;
+  long long cap = 0;
+  double cutoff = 0;
+  // graphs
+  std::map<long long, cudaGraphExec_t> graphs;
+  // instrumentation
+  bool instr = false;
+  std::vector<cudaEvent_t> events;
+  double t_ms[4] = {0, 0, 0, 0};
+  long long t_cnt[4] = {0, 0, 0, 0};
+  // nccl
+  ncclComm_t comm = nullptr;
+  long long steps_done = 0;
+  long long rebuild_host = 0;
+
+  bool collide() const { return env_set && env.self_collision && nsurf > 0; }
+  int launches_per_step() const {
+    int k = 3;  // clock, bonds, integrate
+    if (collide()) k += 2;
+    if (nranks > 1) k += 1;  // bonds split in interior + boundary launches
+    return k;
+  }
+  void clear_graphs() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    graphs.clear();
+  }
+};
+
+namespace {
+
+inline size_t rsize(int prec) { return prec == 32 ? 4 : 8; }
+
+// ---------------------------------------------------------------- L1 builder
+vx_status build_topology(vx_lattice* h) {
+  const int nx = h->nx, ny = h->ny, nz = h->nz;
+  auto cell = [&](int i, int j, int k) -> int {
+    if (i < 0 || j < 0 || k < 0 || i >= nx || j >= ny || k >= nz) return 0;
+    return h->cells[(size_t)i + (size_t)nx * ((size_t)j + (size_t)ny * k)];
+  };
+  // external ids: filled cells in x-fastest order (vx_lattice_desc.cells)
+  h->box_of_ext.clear();
+  h->N = 0;
+  h->max_cell = 0;
+  for (int k = 0; k < nz; ++k)
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        int c = h->cells[(size_t)i + (size_t)nx * ((size_t)j + (size_t)ny * k)];
+        if (!c) continue;
+        h->max_cell = std::max(h->max_cell, c);
+        h->box_of_ext.push_back(((long long)i * ny + j) * nz + k);
+      }
+  h->N = (long long)h->box_of_ext.size();
+  // local box meta: material, filled, neighbour mask, surface
+  h->meta_static.assign(h->nloc, 0u);
+  h->nbonds = 0;
+  h->nsurf = 0;
+  h->surf_local.clear();
+  const int di[6] = {-1, 1, 0, 0, 0, 0}, dj[6] = {0, 0, -1, 1, 0, 0}, dk[6] = {0, 0, 0, 0, -1, 1};
+  for (int i = 0; i < nx; ++i)
+    for (int j = 0; j < ny; ++j)
+      for (int k = 0; k < nz; ++k) {
+        const int c = cell(i, j, k);
+        if (!c) continue;
+        uint32_t m = (uint32_t)(c - 1) | M_FILLED;
+        int cnt = 0;
+        for (int s = 0; s < 6; ++s)
+          if (cell(i + di[s], j + dj[s], k + dk[s])) {
+            m |= nb_bit(s);
+            ++cnt;
+            if (s & 1) ++h->nbonds;
+          }
+        if (cnt < 6) {
+          m |= M_SURF;
+          ++h->nsurf;
+        }
+        if (i >= h->xl0 && i < h->xl1) {
+          const uint32_t li = (uint32_t)(((long long)(i - h->xl0) * ny + j) * nz + k);
+          h->meta_static[li] = m;
+          if ((m & M_SURF) && i >= h->x0 && i < h->x1) h->surf_local.push_back((int)li);
+        }
+      }
+  return VX_OK;
+}
+
+template <class R> Dev<R> make_dev(vx_lattice* h) {
+  Dev<R> d;
+  d.pos = h->pos.as<typename VT<R>::R4>();
+  d.quat = h->quat.as<typename VT<R>::R4>();
+  d.mom = h->mom.as<typename VT<R>::R4>();
+  d.ang = h->ang.as<typename VT<R>::R2>();
+  d.recA = h->recA.as<typename VT<R>::R4>();
+  d.recB = h->recB.as<typename VT<R>::R4>();
+  d.recC = h->recC.as<R>();
+  d.fext = h->any_ext ? h->fextd.as<typename VT<R>::R4>() : nullptr;
+  d.cf = h->cf.as<typename VT<R>::R4>();
+  d.mat = h->mat.as<MatC<R>>();
+  d.pair = h->pair.as<PairC<R>>();
+  d.clk = h->clk.as<Clock>();
+  d.nmat = (int)h->mats.size();
+  d.nloc = h->nloc;
+  d.sx = h->plane;
+  d.ny = (uint32_t)h->ny;
+  d.nz = (uint32_t)h->nz;
+  d.xl0 = h->xl0;
+  d.l = (R)h->l;
+  d.half_l = (R)(0.5 * h->l);
+  d.dt = (R)h->dt;
+  d.l_d = h->l;
+  d.zbase_d = h->origin[2] - h->env.floor_z;
+  d.floor_on = h->env_set ? h->env.floor_on : 0;
+  d.ground = (h->env_set && h->env.zeta_ground > 0) ? 1 : 0;
+  return d;
+}
+
+inline unsigned grid_of(long long n, int b = 256) { return (unsigned)((n + b - 1) / b); }
+
+vx_status upload_meta(vx_lattice* h) {
+  // static bits + boundary bits -> device, merged with the latch bits
+  std::vector<uint32_t> m(h->meta_static);
+  for (long long e = 0; e < h->N; ++e) {
+    const long long li = h->box_of_ext[e] - h->box_base;
+    if (li < 0 || li >= (long long)h->nloc) continue;
+    m[li] &= ~(M_FIXED | M_EXT);
+    if (!h->fixed.empty() && h->fixed[e]) m[li] |= M_FIXED;
+    if (h->any_ext && (h->fext[3 * e] != 0 || h->fext[3 * e + 1] != 0 || h->fext[3 * e + 2] != 0))
+      m[li] |= M_EXT;
+  }
+  VX_CUDA(cudaMemcpyAsync(h->meta_d.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  if (h->prec == 32)
+    k_merge_meta<float><<<grid_of(h->nloc), 256, 0, h->stream>>>(make_dev<float>(h), h->meta_d.as<uint32_t>(), h->nloc);
+  else
+    k_merge_meta<double><<<grid_of(h->nloc), 256, 0, h->stream>>>(make_dev<double>(h), h->meta_d.as<uint32_t>(), h->nloc);
+  VX_CUDA(cudaGetLastError());
+  // external forces (local box order)
+  if (h->any_ext) {
+    const size_t r4 = 4 * rsize(h->prec);
+    VX_TRY(h->fextd.alloc((size_t)h->nloc * r4));
+    std::vector<double> f4((size_t)h->nloc * 4, 0.0);
+    for (long long e = 0; e < h->N; ++e) {
+      const long long li = h->box_of_ext[e] - h->box_base;
+      if (li < 0 || li >= (long long)h->nloc) continue;
+      for (int c = 0; c < 3; ++c) f4[4 * li + c] = h->fext[3 * e + c];
+    }
+    if (h->prec == 32) {
+      std::vector<float> f(f4.begin(), f4.end());
+      VX_CUDA(cudaMemcpyAsync(h->fextd.p, f.data(), f.size() * 4, cudaMemcpyHostToDevice, h->stream));
+      VX_CUDA(cudaStreamSynchronize(h->stream));
+    } else {
+      VX_CUDA(cudaMemcpyAsync(h->fextd.p, f4.data(), f4.size() * 8, cudaMemcpyHostToDevice, h->stream));
+      VX_CUDA(cudaStreamSynchronize(h->stream));
+    }
+  }
+  VX_CUDA(cudaStreamSynchronize(h->stream));
+  h->clear_graphs();
+  return VX_OK;
+}
+
+// ---------------------------------------------------------------- tables
+struct MatD {
+  double E, nu, rho, cte, mu_s, mu_d, G, m, I;
+};
+MatD mat_d(const vx_material& v, double l) {
+  MatD m{v.E, v.nu, v.rho, v.cte, v.mu_s, v.mu_d, 0, 0, 0};
+  m.G = v.E / (2 * (1 + v.nu));
+  m.m = v.rho * l * l * l;        // voxel mass
+  m.I = m.m * l * l / 6.0;        // R8: solid cube
+  return m;
+}
+// Eq. 1-12 for the pair (a, b)
+void pair_consts(const MatD& a, const MatD& b, double l, double* a1, double* a2, double* b1,
+                 double* b2, double* b3) {
+  const double Ec = 2 * a.E * b.E / (a.E + b.E);   // Eq. 1
+  const double Gc = 2 * a.G * b.G / (a.G + b.G);   // Eq. 2
+  const double A = l * l, I = l * l * l * l / 12.0, J = l * l * l * l / 6.0;  // Eq. 4-5
+  *a1 = Ec * A / l;                                 // Eq. 8
+  *a2 = Gc * J / l;                                 // Eq. 9
+  *b1 = 12 * Ec * I / (l * l * l);                  // Eq. 10
+  *b2 = 6 * Ec * I / (l * l);                       // Eq. 11
+  *b3 = 2 * Ec * I / l;                             // Eq. 12
+}
+
+template <class R> vx_status upload_tables(vx_lattice* h) {
+  const int n = (int)h->mats.size();
+  const double l = h->l, dt = h->dt;
+  const vx_env& e = h->env;
+  std::vector<MatC<R>> mc(n);
+  std::vector<PairC<R>> pc((size_t)n * n);
+  std::vector<MatD> md(n);
+  for (int i = 0; i < n; ++i) md[i] = mat_d(h->mats[i], l);
+  for (int i = 0; i < n; ++i) {
+    const MatD& m = md[i];
+    MatC<R>& c = mc[i];
+    c.m = (R)m.m;
+    c.inv_m = (R)(1.0 / m.m);
+    c.inv_I = (R)(1.0 / m.I);
+    c.dt_m = (R)(dt / m.m);
+    c.dt_I = (R)(dt / m.I);
+    c.mg = (R)(m.m * e.gravity);
+    c.cgt = (R)(2 * e.zeta_ground * std::sqrt(m.m * m.E * l));
+    c.cgr = (R)(2 * e.zeta_ground * std::sqrt(m.I * m.G * l * l * l / 6.0));
+    c.kf = (R)(m.E * l);
+    c.cfl = (R)(2 * e.zeta_col * std::sqrt(m.m * m.E * l));
+    c.alpha = (R)m.cte;
+    c.mu_s = (R)m.mu_s;
+    c.mu_d = (R)m.mu_d;
+    c.kc = (R)(m.E * l);
+    c.pad = (R)0;
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double a1, a2, b1, b2, b3;
+      pair_consts(md[i], md[j], l, &a1, &a2, &b1, &b2, &b3);
+      PairC<R>& p = pc[(size_t)i * n + j];
+      p.a1 = (R)a1; p.a2 = (R)a2; p.b1 = (R)b1; p.b2 = (R)b2; p.b3 = (R)b3;
+      p.alpha_mean = (R)(0.5 * (md[i].cte + md[j].cte));
+      const double mmin = std::min(md[i].m, md[j].m), Imin = std::min(md[i].I, md[j].I);
+      p.ct = (R)(2 * e.zeta_bond * std::sqrt(mmin * a1));   // Eq. 34, R10
+      p.cr = (R)(2 * e.zeta_bond * std::sqrt(Imin * a2));   // Eq. 35, R11
+    }
+  VX_TRY(h->mat.alloc(mc.size() * sizeof(MatC<R>)));
+  VX_TRY(h->pair.alloc(pc.size() * sizeof(PairC<R>)));
+  VX_CUDA(cudaMemcpyAsync(h->mat.p, mc.data(), mc.size() * sizeof(MatC<R>), cudaMemcpyHostToDevice, h->stream));
+  VX_CUDA(cudaMemcpyAsync(h->pair.p, pc.data(), pc.size() * sizeof(PairC<R>), cudaMemcpyHostToDevice, h->stream));
+  VX_CUDA(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+// K2: stable timestep from a device max-reduction (Eq. 31-32, R9)
+template <class R> vx_status compute_dt(vx_lattice* h) {
+  const int n = (int)h->mats.size();
+  std::vector<MatD> md(n);
+  for (int i = 0; i < n; ++i) md[i] = mat_d(h->mats[i], h->l);
+  std::vector<double> pw((size_t)n * n), mw(n);
+  for (int i = 0; i < n; ++i) {
+    mw[i] = md[i].E * h->l / md[i].m;
+    for (int j = 0; j < n; ++j) {
+      double a1, a2, b1, b2, b3;
+      pair_consts(md[i], md[j], h->l, &a1, &a2, &b1, &b2, &b3);
+      pw[(size_t)i * n + j] = a1 / std::min(md[i].m, md[j].m);
+    }
+  }
+  VX_TRY(h->pair_w2.alloc(pw.size() * 8));
+  VX_TRY(h->mat_w2.alloc(mw.size() * 8));
+  VX_CUDA(cudaMemcpyAsync(h->pair_w2.p, pw.data(), pw.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  VX_CUDA(cudaMemcpyAsync(h->mat_w2.p, mw.data(), mw.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  Clock* c = h->clk.as<Clock>();
+  VX_CUDA(cudaMemsetAsync(&c->w2_bond_bits, 0, 16, h->stream));
+  k_dt<R><<<grid_of(h->nloc), 256, 0, h->stream>>>(h->pos.as<typename VT<R>::R4>(), 0u, h->nloc,
+                                                   h->plane, (uint32_t)h->nz, h->pair_w2.as<double>(),
+                                                   h->mat_w2.as<double>(), n, c);
+  VX_CUDA(cudaGetLastError());
+  unsigned long long bits[2];
+  VX_CUDA(cudaMemcpyAsync(bits, &c->w2_bond_bits, 16, cudaMemcpyDeviceToHost, h->stream));
+  VX_CUDA(cudaStreamSynchronize(h->stream));
+  double wb, wv;
+  std::memcpy(&wb, &bits[0], 8);
+  std::memcpy(&wv, &bits[1], 8);
+  if (h->nranks > 1) {
+    double* tmp = nullptr;
+    VX_CUDA(cudaMalloc(&tmp, 16));
+    double hv[2] = {wb, wv};
+    VX_CUDA(cudaMemcpy(tmp, hv, 16, cudaMemcpyHostToDevice));
+    VX_NCCL(ncclAllReduce(tmp, tmp, 2, ncclDouble, ncclMax, h->comm, h->stream));
+    VX_CUDA(cudaMemcpyAsync(hv, tmp, 16, cudaMemcpyDeviceToHost, h->stream));
+    VX_CUDA(cudaStreamSynchronize(h->stream));
+    cudaFree(tmp);
+    wb = hv[0];
+    wv = hv[1];
+  }
+  // omega_0m: max over bonds; a lattice without bonds falls back to E l / m
+  h->w2max = h->nbonds > 0 ? wb : wv;
+  return VX_OK;
+}
+
+void update_dt(vx_lattice* h) {
+  const double s = h->env_set ? h->env.dt_safety : 1.0;
+  h->dt = h->w2max > 0 ? s / (2 * kPi * std::sqrt(h->w2max)) : 0.0;
+}
+
+vx_status setup_collision(vx_lattice* h) {
+  const int S = (int)h->surf_local.size();
+  VX_TRY(h->surf_d.alloc((size_t)std::max(S, 1) * 4));
+  if (S) VX_CUDA(cudaMemcpy(h->surf_d.p, h->surf_local.data(), (size_t)S * 4, cudaMemcpyHostToDevice));
+  int H = 1024;
+  while (H < 2 * S) H <<= 1;
+  h->H = H;
+  h->cap = std::max<long long>(1 << 16, 128LL * S);
+  VX_TRY(h->cellh.alloc((size_t)std::max(S, 1) * sizeof(int4)));
+  VX_TRY(h->bcount.alloc((size_t)H * 4));
+  VX_TRY(h->bstart.alloc((size_t)(H + 1) * 4));
+  VX_TRY(h->bitems.alloc((size_t)std::max(S, 1) * 4));
+  VX_TRY(h->rowptr.alloc((size_t)(S + 1) * 4));
+  VX_TRY(h->col.alloc((size_t)h->cap * 4));
+  VX_TRY(h->cf.alloc((size_t)h->nloc * 4 * rsize(h->prec)));
+  VX_CUDA(cudaMemset(h->rowptr.p, 0, (size_t)(S + 1) * 4));
+  VX_CUDA(cudaMemset(h->cf.p, 0, h->cf.bytes));
+  // cutoff = 2 r_max + horizon, r_max = (l/2)(1 + max|alpha| |T_amp|)
+  double amax = 0;
+  for (auto& m : h->mats) amax = std::max(amax, std::fabs(m.cte));
+  const double rmax = 0.5 * h->l * (1 + amax * std::fabs(h->env.T_amp));
+  h->cutoff = 2 * rmax + h->env.horizon_voxels * h->l;
+  return VX_OK;
+}
+
+vx_status prepare(vx_lattice* h) {
+  if (!h->mats_set) return fail(VX_ERR_STATE, "vx_set_materials has not been called");
+  if (!h->env_set) return fail(VX_ERR_STATE, "vx_set_environment has not been called");
+  if (h->tables_dirty) {
+    update_dt(h);
+    if (h->prec == 32) VX_TRY(upload_tables<float>(h));
+    else VX_TRY(upload_tables<double>(h));
+    if (h->collide()) VX_TRY(setup_collision(h));
+    h->tables_dirty = false;
+    h->clear_graphs();
+  }
+  return VX_OK;
+}
+
+// ---------------------------------------------------------------- one step
+template <class R> void launch_bonds(vx_lattice* h, const Dev<R>& d, int p0, int p1) {
+  if (p1 <= p0) return;
+  const uint32_t beg = (uint32_t)(p0 - h->xl0) * h->plane, end = (uint32_t)(p1 - h->xl0) * h->plane;
+  k_bonds<R><<<grid_of(end - beg), 256, 0, h->stream>>>(d, beg, end);
+}
+
+template <class R> vx_status halo_exchange(vx_lattice* h) {
+  // ghost planes <- neighbours' boundary planes (state S_n), on comm_stream
+  const size_t pl = h->plane;
+  const size_t r = rsize(h->prec);
+  struct Arr { char* base; size_t esz; } arrs[4] = {
+      {h->pos.as<char>(), 4 * r}, {h->quat.as<char>(), 4 * r}, {h->mom.as<char>(), 4 * r},
+      {h->ang.as<char>(), 2 * r}};
+  VX_NCCL(ncclGroupStart());
+  for (auto& a : arrs) {
+    const size_t bytes = pl * a.esz;
+    if (h->x0 > 0) {   // left neighbour: send my first owned plane, receive ghost left
+      char* mine = a.base + (size_t)(h->x0 - h->xl0) * pl * a.esz;
+      char* ghost = a.base;
+      VX_NCCL(ncclSend(mine, bytes, ncclInt8, h->rank - 1, h->comm, h->comm_stream));
+      VX_NCCL(ncclRecv(ghost, bytes, ncclInt8, h->rank - 1, h->comm, h->comm_stream));
+    }
+    if (h->x1 < h->nx) {   // right neighbour
+      char* mine = a.base + (size_t)(h->x1 - 1 - h->xl0) * pl * a.esz;
+      char* ghost = a.base + (size_t)(h->x1 - h->xl0) * pl * a.esz;
+      VX_NCCL(ncclSend(mine, bytes, ncclInt8, h->rank + 1, h->comm, h->comm_stream));
+      VX_NCCL(ncclRecv(ghost, bytes, ncclInt8, h->rank + 1, h->comm, h->comm_stream));
+    }
+  }
+  VX_NCCL(ncclGroupEnd());
+  return VX_OK;
+}
+
+template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
+  const Dev<R> d = make_dev<R>(h);
+  const bool col = h->collide();
+  if (ev) VX_CUDA(cudaEventRecord(ev[0], h->stream));
+  ClockArgs ca{h->clk.as<Clock>(), h->dt, h->env.T_amp, h->env.T_freq, h->env.T_phase,
+               0.5 * h->env.horizon_voxels * h->l, col ? 1 : 0, h->prec};
+  k_clock<<<1, 32, 0, h->stream>>>(ca);
+  if (col) {
+    BroadArgs b{h->surf_d.as<int>(), (int)h->surf_local.size(), h->cellh.as<int4>(),
+                h->bcount.as<int>(), h->bstart.as<int>(), h->bitems.as<int>(),
+                h->rowptr.as<int>(), h->col.as<int>(), h->cap, h->H, h->clk.as<Clock>()};
+    const double hc = h->cutoff * 1.001;
+    k_broadphase<R><<<1, 1024, 0, h->stream>>>(d, b, h->origin[0], h->origin[1], h->origin[2],
+                                               (R)hc, (R)(h->cutoff * h->cutoff));
+    const int S = (int)h->surf_local.size();
+    if (S)
+      k_contact<R><<<grid_of(S), 256, 0, h->stream>>>(d, h->surf_d.as<int>(), S, h->rowptr.as<int>(),
+                                                      h->col.as<int>(), (R)h->env.zeta_col);
+  }
+  if (ev) VX_CUDA(cudaEventRecord(ev[1], h->stream));
+  if (h->nranks == 1) {
+    launch_bonds<R>(h, d, h->xl0, h->xl1);
+  } else {
+    // halo of S_n on the comm stream overlapped with the interior bonds
+    VX_CUDA(cudaEventRecord(h->ev_k4, h->stream));
+    VX_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_k4, 0));
+    VX_TRY(halo_exchange<R>(h));
+    VX_CUDA(cudaEventRecord(h->ev_halo, h->comm_stream));
+    launch_bonds<R>(h, d, h->x0, h->x1 - 1);
+    VX_CUDA(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+    if (h->xl0 < h->x0) launch_bonds<R>(h, d, h->xl0, h->x0);
+    launch_bonds<R>(h, d, h->x1 - 1, h->x1);
+  }
+  if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
+  const uint32_t beg = (uint32_t)(h->x0 - h->xl0) * h->plane, end = (uint32_t)(h->x1 - h->xl0) * h->plane;
+  if (col)
+    k_integrate<R, true><<<grid_of(end - beg), 256, 0, h->stream>>>(d, beg, end, h->ext_of_local.as<uint32_t>());
+  else
+    k_integrate<R, false><<<grid_of(end - beg), 256, 0, h->stream>>>(d, beg, end, h->ext_of_local.as<uint32_t>());
+  if (ev) VX_CUDA(cudaEventRecord(ev[3], h->stream));
+  VX_CUDA(cudaGetLastError());
+  return VX_OK;
+}
+
+template <class R> vx_status run_steps(vx_lattice* h, long long n) {
+  if (h->instr) {
+    const size_t need = (size_t)n * 4;
+    while (h->events.size() < need) {
+      cudaEvent_t e;
+      VX_CUDA(cudaEventCreate(&e));
+      h->events.push_back(e);
+    }
+    for (long long s = 0; s < n; ++s) VX_TRY(enqueue_step<R>(h, &h->events[(size_t)s * 4]));
+    VX_CUDA(cudaStreamSynchronize(h->stream));
+    for (long long s = 0; s < n; ++s) {
+      cudaEvent_t* e = &h->events[(size_t)s * 4];
+      float a, b, c, t;
+      VX_CUDA(cudaEventElapsedTime(&a, e[1], e[2]));
+      VX_CUDA(cudaEventElapsedTime(&b, e[2], e[3]));
+      VX_CUDA(cudaEventElapsedTime(&c, e[0], e[1]));
+      VX_CUDA(cudaEventElapsedTime(&t, e[0], e[3]));
+      h->t_ms[0] += a; h->t_ms[1] += b; h->t_ms[2] += c; h->t_ms[3] += t;
+      h->t_cnt[0] += h->nranks > 1 ? 3 : 1;
+      h->t_cnt[1] += 1;
+      h->t_cnt[2] += h->collide() ? 3 : 1;
+      h->t_cnt[3] += h->launches_per_step();
+    }
+    return VX_OK;
+  }
+  // CUDA graphs of G steps; the remainder is captured as its own graph
+  const long long G = 32;
+  long long left = n;
+  while (left > 0) {
+    const long long g = left >= G ? G : left;
+    auto it = h->graphs.find(g);
+    if (it == h->graphs.end()) {
+      cudaGraph_t graph;
+      VX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+      vx_status st = VX_OK;
+      for (long long s = 0; s < g && st == VX_OK; ++s) st = enqueue_step<R>(h, nullptr);
+      cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+      if (st != VX_OK) return st;
+      if (ce != cudaSuccess) return fail(VX_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+      cudaGraphExec_t ex;
+      VX_CUDA(cudaGraphInstantiate(&ex, graph, 0));
+      cudaGraphDestroy(graph);
+      it = h->graphs.emplace(g, ex).first;
+    }
+    VX_CUDA(cudaGraphLaunch(it->second, h->stream));
+    left -= g;
+  }
+  VX_CUDA(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+vx_status check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(VX_ERR_NO_DEVICE, "no CUDA device visible (no CPU fallback)");
+  }
+  return VX_OK;
+}
+
+vx_status set_device(const vx_lattice* h) {
+  VX_CUDA(cudaSetDevice(h->device));
+  return VX_OK;
+}
+
+vx_status read_box(vx_lattice* h, double* boxbuf);
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+const char* vx_last_error(void) { return g_err.c_str(); }
+int32_t vx_abi_version(void) { return VOXSIM_ABI_VERSION; }
+
+vx_status vx_nccl_unique_id(void* out128) {
+  if (!out128) return fail(VX_ERR_INVALID_ARG, "out128 is NULL");
+  ncclUniqueId id;
+  VX_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, 128);
+  return VX_OK;
+}
+
+vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
+  if (!out) return fail(VX_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!desc || !desc->cells) return fail(VX_ERR_INVALID_ARG, "desc or desc->cells is NULL");
+  if (desc->nx < 1 || desc->ny < 1 || desc->nz < 1)
+    return fail(VX_ERR_INVALID_ARG, "nx, ny, nz must be >= 1");
+  if (!(desc->lattice_dim > 0) || !std::isfinite(desc->lattice_dim))
+    return fail(VX_ERR_INVALID_ARG, "lattice_dim must be > 0");
+  if (desc->precision != 32 && desc->precision != 64)
+    return fail(VX_ERR_INVALID_ARG, "precision must be 32 or 64");
+  if (desc->nranks < 1 || desc->rank < 0 || desc->rank >= desc->nranks)
+    return fail(VX_ERR_INVALID_ARG, "bad rank / nranks");
+  if (desc->nranks > desc->nx) return fail(VX_ERR_INVALID_ARG, "nranks > nx (empty slab)");
+  if (desc->nranks > 1 && !desc->nccl_id) return fail(VX_ERR_INVALID_ARG, "nccl_id is NULL");
+  const long long cells = (long long)desc->nx * desc->ny * desc->nz;
+  if (cells >= (1LL << 32)) return fail(VX_ERR_INVALID_ARG, "workspace too large (>= 2^32 cells)");
+  VX_TRY(check_device());
+  vx_lattice* h = new vx_lattice();
+  h->nx = desc->nx; h->ny = desc->ny; h->nz = desc->nz;
+  h->l = desc->lattice_dim;
+  for (int c = 0; c < 3; ++c) h->origin[c] = desc->origin[c];
+  h->prec = desc->precision;
+  h->device = desc->device; h->rank = desc->rank; h->nranks = desc->nranks;
+  h->cells.assign(desc->cells, desc->cells + cells);
+  h->x0 = (int)((long long)h->rank * h->nx / h->nranks);
+  h->x1 = (int)((long long)(h->rank + 1) * h->nx / h->nranks);
+  h->xl0 = std::max(h->x0 - 1, 0);
+  h->xl1 = std::min(h->x1 + 1, h->nx);
+  h->plane = (uint32_t)((long long)h->ny * h->nz);
+  h->nloc = (uint32_t)((long long)(h->xl1 - h->xl0) * h->plane);
+  h->box_base = (long long)h->xl0 * h->plane;
+  h->nbox = (long long)h->nx * h->plane;
+  auto bail = [&](vx_status s) { std::string m = g_err; vx_destroy(h); g_err = m; return s; };
+  vx_status s = set_device(h);
+  if (s != VX_OK) return bail(s);
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_k4, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(VX_ERR_CUDA, "stream/event creation failed"));
+  s = build_topology(h);
+  if (s != VX_OK) return bail(s);
+  const size_t r = rsize(h->prec), n = h->nloc;
+  if ((s = h->pos.alloc(n * 4 * r)) || (s = h->quat.alloc(n * 4 * r)) || (s = h->mom.alloc(n * 4 * r)) ||
+      (s = h->ang.alloc(n * 2 * r)) || (s = h->recA.alloc(3 * n * 4 * r)) ||
+      (s = h->recB.alloc(3 * n * 4 * r)) || (s = h->recC.alloc(3 * n * r)) ||
+      (s = h->clk.alloc(sizeof(Clock))) || (s = h->meta_d.alloc(n * 4)) ||
+      (s = h->box_of_ext_d.alloc((size_t)std::max<long long>(h->N, 1) * 8)) ||
+      (s = h->ext_of_local.alloc(n * 4)))
+    return bail(s);
+  {
+    std::vector<uint32_t> eol(n, 0xffffffffu);
+    for (long long e = 0; e < h->N; ++e) {
+      const long long li = h->box_of_ext[e] - h->box_base;
+      if (li >= 0 && li < (long long)n) eol[li] = (uint32_t)e;
+    }
+    if (cudaMemcpy(h->ext_of_local.p, eol.data(), n * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(VX_ERR_CUDA, "upload failed"));
+  }
+  // initial state: at rest on the lattice sites, identity orientation
+  if (cudaMemset(h->pos.p, 0, h->pos.bytes) != cudaSuccess || cudaMemset(h->mom.p, 0, h->mom.bytes) != cudaSuccess ||
+      cudaMemset(h->ang.p, 0, h->ang.bytes) != cudaSuccess || cudaMemset(h->recA.p, 0, h->recA.bytes) != cudaSuccess ||
+      cudaMemset(h->recB.p, 0, h->recB.bytes) != cudaSuccess || cudaMemset(h->recC.p, 0, h->recC.bytes) != cudaSuccess)
+    return bail(fail(VX_ERR_CUDA, "memset failed"));
+  {
+    std::vector<char> q(h->quat.bytes, 0);
+    for (size_t i = 0; i < n; ++i) {
+      if (r == 4) { float one = 1.f; std::memcpy(&q[i * 16 + 12], &one, 4); }
+      else { double one = 1.0; std::memcpy(&q[i * 32 + 24], &one, 8); }
+    }
+    if (cudaMemcpy(h->quat.p, q.data(), q.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(VX_ERR_CUDA, "upload failed"));
+  }
+  Clock c0{};
+  c0.err = ~0ULL;
+  c0.force_rebuild = 1;
+  if (cudaMemcpy(h->clk.p, &c0, sizeof c0, cudaMemcpyHostToDevice) != cudaSuccess ||
+      (h->N && cudaMemcpy(h->box_of_ext_d.p, h->box_of_ext.data(), (size_t)h->N * 8, cudaMemcpyHostToDevice) != cudaSuccess))
+    return bail(fail(VX_ERR_CUDA, "upload failed"));
+  h->fixed.assign((size_t)h->N, 0);
+  h->fext.assign((size_t)h->N * 3, 0.0);
+  if ((s = upload_meta(h)) != VX_OK) return bail(s);
+  if (h->nranks > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, desc->nccl_id, sizeof id);
+    ncclResult_t nr = ncclCommInitRank(&h->comm, h->nranks, id, h->rank);
+    if (nr != ncclSuccess) return bail(fail(VX_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(nr)));
+  }
+  *out = h;
+  return VX_OK;
+}
+
+void vx_destroy(vx_lattice* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  h->clear_graphs();
+  for (auto e : h->events) cudaEventDestroy(e);
+  if (h->comm) ncclCommDestroy(h->comm);
+  if (h->ev_k4) cudaEventDestroy(h->ev_k4);
+  if (h->ev_halo) cudaEventDestroy(h->ev_halo);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+  delete h;
+}
+
+vx_status vx_set_materials(vx_lattice* h, const vx_material* p, int32_t n) {
+  if (!h || !p || n < 1 || n > 255) return fail(VX_ERR_INVALID_ARG, "bad palette (need 1..255 materials)");
+  for (int i = 0; i < n; ++i) {
+    const vx_material& m = p[i];
+    if (!(m.E > 0) || !(m.rho > 0) || !(m.nu > -1 && m.nu < 0.5) || !(m.mu_d >= 0) ||
+        !(m.mu_s >= m.mu_d) || !std::isfinite(m.E) || !std::isfinite(m.rho) || !std::isfinite(m.cte))
+      return fail(VX_ERR_INVALID_ARG, "material " + std::to_string(i) +
+                                          " violates E>0, rho>0, -1<nu<0.5, mu_s>=mu_d>=0");
+  }
+  if (h->max_cell > n)
+    return fail(VX_ERR_OUT_OF_RANGE, "a cell references material " + std::to_string(h->max_cell) +
+                                         " of a " + std::to_string(n) + "-entry palette");
+  VX_TRY(set_device(h));
+  h->mats.assign(p, p + n);
+  if (h->prec == 32) VX_TRY(compute_dt<float>(h));
+  else VX_TRY(compute_dt<double>(h));
+  h->mats_set = true;
+  h->tables_dirty = true;
+  Clock* c = h->clk.as<Clock>();
+  int one = 1;
+  VX_CUDA(cudaMemcpy(&c->force_rebuild, &one, 4, cudaMemcpyHostToDevice));
+  update_dt(h);
+  return VX_OK;
+}
+
+vx_status vx_set_environment(vx_lattice* h, const vx_env* e) {
+  if (!h || !e) return fail(VX_ERR_INVALID_ARG, "NULL argument");
+  auto ratio_ok = [](double z) { return z >= 0 && z <= 1; };
+  if (!ratio_ok(e->zeta_bond) || !ratio_ok(e->zeta_ground) || !ratio_ok(e->zeta_col))
+    return fail(VX_ERR_INVALID_ARG, "damping ratios must lie in [0,1] (App. B)");
+  if (!(e->dt_safety > 0 && e->dt_safety <= 1)) return fail(VX_ERR_INVALID_ARG, "dt_safety must be in (0,1]");
+  if (e->self_collision && !(e->horizon_voxels > 0))
+    return fail(VX_ERR_INVALID_ARG, "horizon_voxels must be > 0");
+  if (e->self_collision && h->nranks > 1)
+    return fail(VX_ERR_INVALID_ARG, "self collision with nranks > 1 is not supported yet");
+  const double v[] = {e->gravity, e->floor_z, e->T_ref, e->T_amp, e->T_freq, e->T_phase};
+  for (double x : v)
+    if (!std::isfinite(x)) return fail(VX_ERR_INVALID_ARG, "non-finite environment value");
+  VX_TRY(set_device(h));
+  h->env = *e;
+  h->env_set = true;
+  h->tables_dirty = true;
+  update_dt(h);
+  Clock* c = h->clk.as<Clock>();
+  int one = 1;
+  VX_CUDA(cudaMemcpy(&c->force_rebuild, &one, 4, cudaMemcpyHostToDevice));
+  h->clear_graphs();
+  return VX_OK;
+}
+
+vx_status vx_set_boundary(vx_lattice* h, const uint8_t* fixed, const double* f_ext) {
+  if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
+  VX_TRY(set_device(h));
+  h->fixed.assign((size_t)h->N, 0);
+  h->fext.assign((size_t)h->N * 3, 0.0);
+  if (fixed) std::copy(fixed, fixed + h->N, h->fixed.begin());
+  h->any_ext = false;
+  if (f_ext) {
+    for (long long i = 0; i < 3 * h->N; ++i) {
+      if (!std::isfinite(f_ext[i])) return fail(VX_ERR_INVALID_ARG, "non-finite external force");
+      h->fext[i] = f_ext[i];
+      h->any_ext |= f_ext[i] != 0;
+    }
+  }
+  return upload_meta(h);
+}
+
+vx_status vx_add_region(vx_lattice* h, int32_t kind, const double o[3], const double sz[3],
+                        const double force[3]) {
+  if (!h || !o || !sz) return fail(VX_ERR_INVALID_ARG, "NULL argument");
+  if (kind != 0 && kind != 1) return fail(VX_ERR_INVALID_ARG, "kind must be 0 (fixed) or 1 (forced)");
+  if (kind == 1 && !force) return fail(VX_ERR_INVALID_ARG, "forced region needs a force");
+  for (int d = 0; d < 3; ++d)
+    if (!(o[d] >= 0 && o[d] <= 1 && sz[d] >= 0 && o[d] + sz[d] <= 1 + 1e-12))
+      return fail(VX_ERR_INVALID_ARG, "region must lie within the workspace fractions [0,1]");
+  VX_TRY(set_device(h));
+  const int dims[3] = {h->nx, h->ny, h->nz};
+  std::vector<long long> hit;
+  for (long long e = 0; e < h->N; ++e) {
+    const long long g = h->box_of_ext[e];
+    const long long idx[3] = {g / h->plane, (g / h->nz) % h->ny, g % h->nz};
+    bool in = true;
+    for (int d = 0; d < 3 && in; ++d) {
+      const double lo = o[d] * dims[d], hi = (o[d] + sz[d]) * dims[d];
+      const double c0 = (double)idx[d], c1 = c0 + 1.0;
+      in = (hi > lo) ? (std::max(lo, c0) < std::min(hi, c1)) : (c0 <= lo && lo <= c1);
+    }
+    if (in) hit.push_back(e);
+  }
+  if (kind == 0) {
+    for (long long e : hit) h->fixed[e] = 1;
+  } else if (!hit.empty()) {
+    const double inv = 1.0 / (double)hit.size();
+    for (long long e : hit)
+      for (int c = 0; c < 3; ++c) {
+        h->fext[3 * e + c] += force[c] * inv;
+        h->any_ext |= h->fext[3 * e + c] != 0;
+      }
+  }
+  return upload_meta(h);
+}
+
+vx_status vx_set_state(vx_lattice* h, const double* pos, const double* quat, const double* lin,
+                       const double* ang, const uint8_t* latch) {
+  if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
+  VX_TRY(set_device(h));
+  const long long N = h->N;
+  if (N == 0) return VX_OK;
+  DevBuf b;
+  const size_t off[5] = {0, (size_t)N * 3, (size_t)N * 7, (size_t)N * 10, (size_t)N * 13};
+  VX_TRY(b.alloc((size_t)N * 13 * 8 + (size_t)N));
+  double* bd = b.as<double>();
+  uint8_t* bl = reinterpret_cast<uint8_t*>(bd + off[4]);
+  if (pos) VX_CUDA(cudaMemcpyAsync(bd + off[0], pos, (size_t)N * 24, cudaMemcpyHostToDevice, h->stream));
+  if (quat) VX_CUDA(cudaMemcpyAsync(bd + off[1], quat, (size_t)N * 32, cudaMemcpyHostToDevice, h->stream));
+  if (lin) VX_CUDA(cudaMemcpyAsync(bd + off[2], lin, (size_t)N * 24, cudaMemcpyHostToDevice, h->stream));
+  if (ang) VX_CUDA(cudaMemcpyAsync(bd + off[3], ang, (size_t)N * 24, cudaMemcpyHostToDevice, h->stream));
+  if (latch) VX_CUDA(cudaMemcpyAsync(bl, latch, (size_t)N, cudaMemcpyHostToDevice, h->stream));
+  const long long* boe = h->box_of_ext_d.as<long long>();
+  if (h->prec == 32)
+    k_scatter_state<float><<<grid_of(N), 256, 0, h->stream>>>(
+        make_dev<float>(h), boe, N, h->box_base, pos ? bd + off[0] : nullptr, quat ? bd + off[1] : nullptr,
+        lin ? bd + off[2] : nullptr, ang ? bd + off[3] : nullptr, latch ? bl : nullptr, h->origin[0],
+        h->origin[1], h->origin[2]);
+  else
+    k_scatter_state<double><<<grid_of(N), 256, 0, h->stream>>>(
+        make_dev<double>(h), boe, N, h->box_base, pos ? bd + off[0] : nullptr, quat ? bd + off[1] : nullptr,
+        lin ? bd + off[2] : nullptr, ang ? bd + off[3] : nullptr, latch ? bl : nullptr, h->origin[0],
+        h->origin[1], h->origin[2]);
+  VX_CUDA(cudaGetLastError());
+  Clock* c = h->clk.as<Clock>();
+  int one = 1;
+  VX_CUDA(cudaMemcpyAsync(&c->force_rebuild, &one, 4, cudaMemcpyHostToDevice, h->stream));
+  VX_CUDA(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+vx_status vx_set_step(vx_lattice* h, int64_t n) {
+  if (!h || n < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
+  VX_TRY(set_device(h));
+  Clock* c = h->clk.as<Clock>();
+  long long v = n;
+  VX_CUDA(cudaMemcpy(&c->next, &v, 8, cudaMemcpyHostToDevice));
+  h->steps_done = n;
+  return VX_OK;
+}
+
+vx_status vx_step(vx_lattice* h, int64_t n) {
+  if (!h || n < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
+  if (n == 0) return VX_OK;
+  VX_TRY(set_device(h));
+  VX_TRY(prepare(h));
+  if (h->N == 0) { h->steps_done += n; return VX_OK; }
+  if (h->prec == 32) VX_TRY(run_steps<float>(h, n));
+  else VX_TRY(run_steps<double>(h, n));
+  h->steps_done += n;
+  Clock c;
+  VX_CUDA(cudaMemcpy(&c, h->clk.p, sizeof c, cudaMemcpyDeviceToHost));
+  unsigned long long err = c.err;
+  int fault = c.fault, overflow = c.overflow;
+  if (h->nranks > 1) {
+    unsigned long long* t = nullptr;
+    VX_CUDA(cudaMalloc(&t, 24));
+    unsigned long long hv[3] = {err, ~0ULL - (unsigned long long)fault, ~0ULL - (unsigned long long)overflow};
+    VX_CUDA(cudaMemcpy(t, hv, 24, cudaMemcpyHostToDevice));
+    VX_NCCL(ncclAllReduce(t, t, 3, ncclUint64, ncclMin, h->comm, h->stream));
+    VX_CUDA(cudaMemcpyAsync(hv, t, 24, cudaMemcpyDeviceToHost, h->stream));
+    VX_CUDA(cudaStreamSynchronize(h->stream));
+    cudaFree(t);
+    err = hv[0];
+    fault = (int)(~0ULL - hv[1]);
+    overflow = (int)(~0ULL - hv[2]);
+  }
+  if (overflow) return fail(VX_ERR_STATE, "contact pair list capacity exceeded");
+  if (fault) return fail(VX_ERR_DIVERGED, "non-positive thermal rest length (S:205)");
+  if (err != ~0ULL) {
+    const long long step = (long long)(err >> 32);
+    const long long ext = (long long)(err & 0xffffffffULL);
+    return fail(VX_ERR_DIVERGED, "diverged: voxel " + std::to_string(ext) + " at step " + std::to_string(step));
+  }
+  return VX_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// Owned planes -> box-ordered fp64 SoA on every rank (ncclBroadcast per rank).
+vx_status read_box(vx_lattice* h, double* boxbuf) {
+  const uint32_t beg = (uint32_t)(h->x0 - h->xl0) * h->plane, end = (uint32_t)(h->x1 - h->xl0) * h->plane;
+  if (h->prec == 32)
+    k_pack_box<float><<<grid_of(end - beg), 256, 0, h->stream>>>(make_dev<float>(h), beg, end, h->box_base,
+                                                                 h->nbox, boxbuf, h->origin[0], h->origin[1], h->origin[2]);
+  else
+    k_pack_box<double><<<grid_of(end - beg), 256, 0, h->stream>>>(make_dev<double>(h), beg, end, h->box_base,
+                                                                  h->nbox, boxbuf, h->origin[0], h->origin[1], h->origin[2]);
+  VX_CUDA(cudaGetLastError());
+  if (h->nranks > 1) {
+    VX_NCCL(ncclGroupStart());
+    for (int r = 0; r < h->nranks; ++r) {
+      const long long x0 = (long long)r * h->nx / h->nranks, x1 = (long long)(r + 1) * h->nx / h->nranks;
+      const size_t cnt = (size_t)((x1 - x0) * h->plane);
+      for (int c = 0; c < 14; ++c) {
+        double* p = boxbuf + (size_t)c * h->nbox + (size_t)x0 * h->plane;
+        VX_NCCL(ncclBroadcast(p, p, cnt, ncclDouble, r, h->comm, h->stream));
+      }
+    }
+    VX_NCCL(ncclGroupEnd());
+  }
+  return VX_OK;
+}
+}  // namespace
+
+extern "C" {
+
+vx_status vx_read_state(vx_lattice* h, double* pos, double* quat, double* lin, double* ang,
+                        uint8_t* latch) {
+  if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
+  VX_TRY(set_device(h));
+  const long long N = h->N;
+  if (N == 0) return VX_OK;
+  DevBuf box, ext;
+  VX_TRY(box.alloc((size_t)h->nbox * 14 * 8));
+  VX_TRY(ext.alloc((size_t)N * 13 * 8 + (size_t)N));
+  VX_TRY(read_box(h, box.as<double>()));
+  double* e = ext.as<double>();
+  uint8_t* el = reinterpret_cast<uint8_t*>(e + (size_t)N * 13);
+  k_box_to_ext<<<grid_of(N), 256, 0, h->stream>>>(box.as<double>(), h->nbox, h->box_of_ext_d.as<long long>(), N,
+                                                  e, e + (size_t)N * 3, e + (size_t)N * 7, e + (size_t)N * 10, el);
+  VX_CUDA(cudaGetLastError());
+  if (pos) VX_CUDA(cudaMemcpyAsync(pos, e, (size_t)N * 24, cudaMemcpyDeviceToHost, h->stream));
+  if (quat) VX_CUDA(cudaMemcpyAsync(quat, e + (size_t)N * 3, (size_t)N * 32, cudaMemcpyDeviceToHost, h->stream));
+  if (lin) VX_CUDA(cudaMemcpyAsync(lin, e + (size_t)N * 7, (size_t)N * 24, cudaMemcpyDeviceToHost, h->stream));
+  if (ang) VX_CUDA(cudaMemcpyAsync(ang, e + (size_t)N * 10, (size_t)N * 24, cudaMemcpyDeviceToHost, h->stream));
+  if (latch) VX_CUDA(cudaMemcpyAsync(latch, el, (size_t)N, cudaMemcpyDeviceToHost, h->stream));
+  VX_CUDA(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+vx_status vx_read_voxels(vx_lattice* h, const int64_t* ids, int64_t n, double* pos, double* quat,
+                         double* lin, double* ang, uint8_t* latch) {
+  if (!h || (n > 0 && !ids) || n < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
+  if (n == 0) return VX_OK;
+  VX_TRY(set_device(h));
+  std::vector<long long> lid((size_t)n), gid((size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= h->N) return fail(VX_ERR_OUT_OF_RANGE, "voxel id out of range");
+    const long long g = h->box_of_ext[ids[i]];
+    const long long x = g / h->plane;
+    if (x < h->x0 || x >= h->x1) return fail(VX_ERR_OUT_OF_RANGE, "voxel not owned by this rank");
+    gid[i] = g;
+    lid[i] = g - h->box_base;
+  }
+  DevBuf ib, ob;
+  VX_TRY(ib.alloc((size_t)n * 16));
+  VX_TRY(ob.alloc((size_t)n * 13 * 8 + (size_t)n));
+  long long* dl = ib.as<long long>();
+  VX_CUDA(cudaMemcpyAsync(dl, lid.data(), (size_t)n * 8, cudaMemcpyHostToDevice, h->stream));
+  VX_CUDA(cudaMemcpyAsync(dl + n, gid.data(), (size_t)n * 8, cudaMemcpyHostToDevice, h->stream));
+  double* o = ob.as<double>();
+  uint8_t* ol = reinterpret_cast<uint8_t*>(o + (size_t)n * 13);
+  if (h->prec == 32)
+    k_read_ids<float><<<grid_of(n), 256, 0, h->stream>>>(make_dev<float>(h), dl, dl + n, n, o, o + n * 3, o + n * 7,
+                                                         o + n * 10, ol, h->origin[0], h->origin[1], h->origin[2]);
+  else
+    k_read_ids<double><<<grid_of(n), 256, 0, h->stream>>>(make_dev<double>(h), dl, dl + n, n, o, o + n * 3, o + n * 7,
+                                                          o + n * 10, ol, h->origin[0], h->origin[1], h->origin[2]);
+  VX_CUDA(cudaGetLastError());
+  if (pos) VX_CUDA(cudaMemcpyAsync(pos, o, (size_t)n * 24, cudaMemcpyDeviceToHost, h->stream));
+  if (quat) VX_CUDA(cudaMemcpyAsync(quat, o + n * 3, (size_t)n * 32, cudaMemcpyDeviceToHost, h->stream));
+  if (lin) VX_CUDA(cudaMemcpyAsync(lin, o + n * 7, (size_t)n * 24, cudaMemcpyDeviceToHost, h->stream));
+  if (ang) VX_CUDA(cudaMemcpyAsync(ang, o + n * 10, (size_t)n * 24, cudaMemcpyDeviceToHost, h->stream));
+  if (latch) VX_CUDA(cudaMemcpyAsync(latch, ol, (size_t)n, cudaMemcpyDeviceToHost, h->stream));
+  VX_CUDA(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+double vx_dt(const vx_lattice* h) { return h ? h->dt : 0.0; }
+int64_t vx_num_voxels(const vx_lattice* h) { return h ? h->N : -1; }
+int64_t vx_num_bonds(const vx_lattice* h) { return h ? h->nbonds : -1; }
+int64_t vx_num_surface(const vx_lattice* h) { return h ? h->nsurf : -1; }
+int64_t vx_steps_done(const vx_lattice* h) { return h ? h->steps_done : -1; }
+
+int64_t vx_num_contact_pairs(const vx_lattice* h) {
+  if (!h || !h->clk.p) return -1;
+  Clock c;
+  if (cudaMemcpy(&c, h->clk.p, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return c.npairs;
+}
+int64_t vx_num_rebuilds(const vx_lattice* h) {
+  if (!h || !h->clk.p) return -1;
+  Clock c;
+  if (cudaMemcpy(&c, h->clk.p, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return c.rebuilds;
+}
+int32_t vx_owned_planes(const vx_lattice* h, int32_t* xb, int32_t* xe) {
+  if (!h) return -1;
+  if (xb) *xb = h->x0;
+  if (xe) *xe = h->x1;
+  return h->x1 - h->x0;
+}
+void* vx_stream(const vx_lattice* h) { return h ? (void*)h->stream : nullptr; }
+
+vx_status vx_set_instrumentation(vx_lattice* h, int32_t on) {
+  if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
+  h->instr = on != 0;
+  for (int i = 0; i < 4; ++i) { h->t_ms[i] = 0; h->t_cnt[i] = 0; }
+  return VX_OK;
+}
+vx_status vx_kernel_times(vx_lattice* h, double out_ms[4], int64_t counts[4]) {
+  if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
+  for (int i = 0; i < 4; ++i) {
+    if (out_ms) out_ms[i] = h->t_ms[i];
+    if (counts) counts[i] = h->t_cnt[i];
+  }
+  return VX_OK;
+}
+int32_t vx_launches_per_step(const vx_lattice* h) { return h ? h->launches_per_step() : -1; }
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// vx_common.cuh -- device types, SoA layout and small vector/quaternion math
+// for the voxel stepper (arXiv:1212.2845).  Product path: shares nothing with
+// oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vx {
+
+// ---------------------------------------------------------------- layout
+// Per-voxel state, box-indexed (internal id = ((i - xl0) * ny + j) * nz + k,
+// x slowest so an x-slab and each x-plane is one contiguous range):
+//   pos  R4 = (u.x, u.y, u.z, meta bits)   u = D - D_rest (displacement)
+//   quat R4 = (x, y, z, w)   (CUDA member order; .w is the scalar part)
+//   mom  R4 = (P.x, P.y, P.z, phi.x)
+//   ang  R2 = (phi.y, phi.z)
+// Bond records per axis a (bond (v, v+e_a) stored at v):
+//   recA R4 = (Fa.x, Fa.y, Fa.z, Ma.x)
+//   recB R4 = (Ma.y, Ma.z, Mb.x, Mb.y)
+//   recC R  = Mb.z
+// meta bits (uint32):
+enum : uint32_t {
+  M_MAT = 0xffu,          // material index (0-based)
+  M_FILLED = 1u << 8,
+  M_FIXED = 1u << 9,
+  M_LATCH = 1u << 10,
+  M_SURF = 1u << 11,
+  M_EXT = 1u << 12,       // has an external force (fext array)
+  M_NB_SHIFT = 16,        // 6 bits: -x,+x,-y,+y,-z,+z
+};
+__host__ __device__ constexpr uint32_t nb_bit(int slot) { return 1u << (M_NB_SHIFT + slot); }
+
+template <class R> struct VT;
+template <> struct VT<float> {
+  using R4 = float4;
+  using R2 = float2;
+  using UB = unsigned int;          // bit pattern type for max-reductions
+};
+template <> struct VT<double> {
+  using R4 = double4;
+  using R2 = double2;
+  using UB = unsigned long long;
+};
+
+__device__ __forceinline__ uint32_t meta_of(float w) { return __float_as_uint(w); }
+__device__ __forceinline__ uint32_t meta_of(double w) {
+  return (uint32_t)(unsigned long long)__double_as_longlong(w);
+}
+__device__ __forceinline__ float meta_as(float, uint32_t m) { return __uint_as_float(m); }
+__device__ __forceinline__ double meta_as(double, uint32_t m) {
+  return __longlong_as_double((long long)(unsigned long long)m);
+}
+__device__ __forceinline__ unsigned int rbits(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ unsigned long long rbits(double x) {
+  return (unsigned long long)__double_as_longlong(x);
+}
+
+// Per-material constants (host fp64, cast to R).
+template <class R> struct MatC {
+  R m, inv_m, inv_I, dt_m, dt_I;  // dt_m = dt/m, dt_I = dt/I
+  R mg;                           // m * g
+  R cgt, cgr;                     // ground damping 2 zeta_g sqrt(m E l), 2 zeta_g sqrt(I G l^3/6)
+  R kf, cfl;                      // floor stiffness E l and damping 2 zeta_col sqrt(m kf)
+  R alpha, mu_s, mu_d;
+  R kc;                           // contact stiffness E l
+  R pad;
+};
+// Per material-pair constants (Eq. 1-12, 34-35, 40).
+template <class R> struct PairC {
+  R a1, a2, b1, b2, b3;
+  R alpha_mean;                   // (alpha_1 + alpha_2) / 2
+  R ct, cr;                       // 2 zeta_b sqrt(m_min a1), 2 zeta_b sqrt(I_min a2)
+};
+
+// ---------------------------------------------------------------- vec3
+template <class R> struct V3 {
+  R x, y, z;
+};
+template <class R> __device__ __forceinline__ V3<R> mk(R x, R y, R z) { return {x, y, z}; }
+template <class R> __device__ __forceinline__ V3<R> operator+(V3<R> a, V3<R> b) {
+  return {a.x + b.x, a.y + b.y, a.z + b.z};
+}
+template <class R> __device__ __forceinline__ V3<R> operator-(V3<R> a, V3<R> b) {
+  return {a.x - b.x, a.y - b.y, a.z - b.z};
+}
+template <class R> __device__ __forceinline__ V3<R> operator*(R s, V3<R> a) {
+  return {s * a.x, s * a.y, s * a.z};
+}
+template <class R> __device__ __forceinline__ V3<R> cross(V3<R> a, V3<R> b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+template <class R> __device__ __forceinline__ R dot(V3<R> a, V3<R> b) {
+  return a.x * b.x + a.y * b.y + a.z * b.z;
+}
+template <class R> __device__ __forceinline__ R comp(V3<R> a, int i) {
+  return i == 0 ? a.x : (i == 1 ? a.y : a.z);
+}
+
+// Rotation matrix of a unit quaternion, split as R = I + Dm with the
+// diagonal of Dm formed without cancellation (-2(y^2+z^2) ...).
+template <class R> struct Rot {
+  R m[3][3];   // full rotation matrix
+  R dd[3];     // m[i][i] - 1
+};
+template <class R> __device__ __forceinline__ Rot<R> rotation(R w, R x, R y, R z) {
+  Rot<R> r;
+  const R two = R(2);
+  r.dd[0] = -two * (y * y + z * z);
+  r.dd[1] = -two * (x * x + z * z);
+  r.dd[2] = -two * (x * x + y * y);
+  r.m[0][0] = R(1) + r.dd[0];
+  r.m[1][1] = R(1) + r.dd[1];
+  r.m[2][2] = R(1) + r.dd[2];
+  r.m[0][1] = two * (x * y - w * z);
+  r.m[0][2] = two * (x * z + w * y);
+  r.m[1][0] = two * (x * y + w * z);
+  r.m[1][2] = two * (y * z - w * x);
+  r.m[2][0] = two * (x * z - w * y);
+  r.m[2][1] = two * (y * z + w * x);
+  return r;
+}
+template <class R> __device__ __forceinline__ V3<R> mul(const Rot<R>& r, V3<R> a) {
+  return {r.m[0][0] * a.x + r.m[0][1] * a.y + r.m[0][2] * a.z,
+          r.m[1][0] * a.x + r.m[1][1] * a.y + r.m[1][2] * a.z,
+          r.m[2][0] * a.x + r.m[2][1] * a.y + r.m[2][2] * a.z};
+}
+template <class R> __device__ __forceinline__ V3<R> mulT(const Rot<R>& r, V3<R> a) {
+  return {r.m[0][0] * a.x + r.m[1][0] * a.y + r.m[2][0] * a.z,
+          r.m[0][1] * a.x + r.m[1][1] * a.y + r.m[2][1] * a.z,
+          r.m[0][2] * a.x + r.m[1][2] * a.y + r.m[2][2] * a.z};
+}
+
+// Cyclic permutation Pi of reading R5: world -> bond frame of axis AX.
+template <int AX, class R> __device__ __forceinline__ V3<R> to_bond(V3<R> a) {
+  if constexpr (AX == 0) return a;
+  else if constexpr (AX == 1) return {a.y, a.z, a.x};
+  else return {a.z, a.x, a.y};
+}
+template <int AX, class R> __device__ __forceinline__ V3<R> to_world(V3<R> a) {
+  if constexpr (AX == 0) return a;
+  else if constexpr (AX == 1) return {a.z, a.x, a.y};
+  else return {a.y, a.z, a.x};
+}
+
+__device__ __forceinline__ float vx_atan2(float y, float x) { return atan2f(y, x); }
+__device__ __forceinline__ double vx_atan2(double y, double x) { return atan2(y, x); }
+__device__ __forceinline__ float vx_sqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double vx_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ void vx_sincos(float a, float* s, float* c) { sincosf(a, s, c); }
+__device__ __forceinline__ void vx_sincos(double a, double* s, double* c) { sincos(a, s, c); }
+__device__ __forceinline__ bool vx_finite(float x) { return isfinite(x); }
+__device__ __forceinline__ bool vx_finite(double x) { return isfinite(x); }
+
+}  // namespace vx

@@ -1,0 +1,696 @@
+// vx_kernels.cuh -- sm_100a kernels of the voxel stepper (arXiv:1212.2845).
+//
+//   k_clock      per-step scalars: t_n, T_n - T_r, motion budget
+//   k_dt         K2: stable timestep max-reduction over bonds (Eq. 31-32)
+//   k_bonds      K3: per-bond loads (Eq. 13-24, 33-35, 39-40)
+//   k_integrate  K4: fixed-order gather (Eq. 25-26), gravity, ground damping,
+//                contacts, floor + friction, integration (Eq. 27-30)
+//   k_broadphase K5: hashed-grid surface-voxel pair list
+//   k_contact    self-collision penalty loads on the shortlist
+// plus state scatter/gather for the C ABI.  Readings: DESIGN.md §3.
+#pragma once
+#include "vx_common.cuh"
+
+namespace vx {
+
+// Device-resident per-lattice scalars (one allocation).
+struct Clock {
+  double dT;                    // T_n - T_ref of the step in flight
+  long long step;               // index n of the step in flight
+  long long next;               // step counter (steps started)
+  double budget;                // accumulated max|V| dt since the last rebuild
+  unsigned long long vmax_bits; // max |V| of the last update (R bits)
+  int rebuild;                  // broadphase runs this step
+  int force_rebuild;            // set by set_state / set_environment
+  unsigned long long err;       // min over ((step << 32) | box id) of diverged voxels
+  int fault;                    // 1: non-positive thermal rest length
+  int overflow;                 // contact pair list capacity exceeded
+  long long npairs;             // pairs a<b in the shortlist
+  long long rebuilds;
+  unsigned long long w2_bond_bits, w2_vox_bits;  // K2 output (double bits)
+};
+
+template <class R> struct Dev {
+  using R4 = typename VT<R>::R4;
+  using R2 = typename VT<R>::R2;
+  R4* pos;
+  R4* quat;
+  R4* mom;
+  R2* ang;
+  R4* recA;   // [3][nloc]
+  R4* recB;   // [3][nloc]
+  R* recC;    // [3][nloc]
+  const R4* fext;
+  R4* cf;     // contact force per voxel (collision only)
+  const MatC<R>* mat;
+  const PairC<R>* pair;
+  Clock* clk;
+  int nmat;
+  uint32_t nloc, sx, ny, nz;
+  int xl0;            // global x of local plane 0
+  R l, half_l, dt;
+  double l_d;         // l in fp64: rest sites D0 = origin + l (ijk + 1/2) are formed
+                      // in fp64 so the fp32 rounding of l never strains the lattice
+  double zbase_d;     // origin_z - floor_z
+  int floor_on, ground;
+};
+
+// ------------------------------------------------------------------ clock
+struct ClockArgs {
+  Clock* clk;
+  double dt, T_amp, T_freq, T_phase;
+  double half_horizon;   // rebuild when budget >= horizon / 2
+  int collide, precision;
+};
+
+__global__ void k_clock(ClockArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Clock* c = a.clk;
+  const long long n = c->next;
+  const double t = (double)n * a.dt;
+  const double PI = 3.14159265358979323846;
+  c->dT = a.T_amp * sin(2 * PI * a.T_freq * t + a.T_phase);
+  c->step = n;
+  c->next = n + 1;
+  if (a.collide) {
+    double vmax = a.precision == 32 ? (double)__uint_as_float((unsigned)c->vmax_bits)
+                                    : __longlong_as_double((long long)c->vmax_bits);
+    c->vmax_bits = 0;
+    double b = c->budget + vmax * a.dt;
+    if (c->force_rebuild || b >= a.half_horizon) {
+      c->rebuild = 1;
+      c->force_rebuild = 0;
+      b = 0;
+    } else {
+      c->rebuild = 0;
+    }
+    c->budget = b;
+  }
+}
+
+// ------------------------------------------------------------------ K2 dt
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// w2 of a bond = a1 / m_min (pair table, fp64); w2 of a voxel = E l / m.
+template <class R>
+__global__ void __launch_bounds__(256) k_dt(const typename VT<R>::R4* pos, uint32_t beg,
+                                            uint32_t end, uint32_t sx, uint32_t nz,
+                                            const double* pair_w2, const double* mat_w2,
+                                            int nmat, Clock* clk) {
+  __shared__ double sb[8], sv[8];
+  const uint32_t id = beg + blockIdx.x * blockDim.x + threadIdx.x;
+  double wb = 0, wv = 0;
+  if (id < end) {
+    uint32_t m = meta_of(pos[id].w);
+    if (m & M_FILLED) {
+      int ma = m & M_MAT;
+      wv = mat_w2[ma];
+      const uint32_t strides[3] = {sx, nz, 1u};
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax)
+        if (m & nb_bit(2 * ax + 1)) {
+          int mb = meta_of(pos[id + strides[ax]].w) & M_MAT;
+          wb = fmax(wb, pair_w2[ma * nmat + mb]);
+        }
+    }
+  }
+  wb = warp_max(wb);
+  wv = warp_max(wv);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { sb[warp] = wb; sv[warp] = wv; }
+  __syncthreads();
+  if (warp == 0) {
+    wb = lane < (int)(blockDim.x >> 5) ? sb[lane] : 0.0;
+    wv = lane < (int)(blockDim.x >> 5) ? sv[lane] : 0.0;
+    wb = warp_max(wb);
+    wv = warp_max(wv);
+    if (lane == 0) {   // positive doubles order like their bit patterns
+      atomicMax(&clk->w2_bond_bits, (unsigned long long)__double_as_longlong(wb));
+      atomicMax(&clk->w2_vox_bits, (unsigned long long)__double_as_longlong(wv));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K3 bonds
+// Voxel a = id (negative side, R4), b = id + stride(AX).  Loads in the frame
+// of a, Eq. 13-24 sign-fixed and negated (R1, R3), back to world
+// (P:206), plus local damping (Eq. 33-35, R10, R11).
+template <int AX, class R>
+__device__ __forceinline__ void bond_one(const Dev<R>& d, uint32_t ia, uint32_t ib,
+                                         const Rot<R>& Ra, const typename VT<R>::R4& qa,
+                                         V3<R> ua, V3<R> Va, V3<R> wa, int mat_a, R dT) {
+  using R4 = typename VT<R>::R4;
+  using R2 = typename VT<R>::R2;
+  const R4 pb = d.pos[ib];
+  const R4 qb = d.quat[ib];
+  const R4 mob = d.mom[ib];
+  const R2 anb = d.ang[ib];
+  const uint32_t mb_meta = meta_of(pb.w);
+  const int mat_b = mb_meta & M_MAT;
+  const PairC<R> c = d.pair[mat_a * d.nmat + mat_b];
+  const MatC<R>& Mb = d.mat[mat_b];
+  const R l = d.l;
+
+  // relative position in a's frame, cancellation-free:
+  //   R^T r - l e = l (R^T e - e) + R^T (u_b - u_a)
+  const V3<R> du = mk(pb.x - ua.x, pb.y - ua.y, pb.z - ua.z);
+  V3<R> t;  // R^T e_AX - e_AX = row AX of (R - I)
+  if constexpr (AX == 0) t = mk(Ra.dd[0], Ra.m[0][1], Ra.m[0][2]);
+  else if constexpr (AX == 1) t = mk(Ra.m[1][0], Ra.dd[1], Ra.m[1][2]);
+  else t = mk(Ra.m[2][0], Ra.m[2][1], Ra.dd[2]);
+  const V3<R> dv = to_bond<AX>(l * t + mulT(Ra, du));
+
+  // relative rotation theta = rotvec(q_a* q_b), w >= 0 (R6, R7)
+  R qw = qa.w * qb.w + qa.x * qb.x + qa.y * qb.y + qa.z * qb.z;
+  R qx = qa.w * qb.x - qa.x * qb.w - qa.y * qb.z + qa.z * qb.y;
+  R qy = qa.w * qb.y + qa.x * qb.z - qa.y * qb.w - qa.z * qb.x;
+  R qz = qa.w * qb.z - qa.x * qb.y + qa.y * qb.x - qa.z * qb.w;
+  if (qw < R(0)) { qw = -qw; qx = -qx; qy = -qy; qz = -qz; }
+  const R s = vx_sqrt(qx * qx + qy * qy + qz * qz);
+  const R k = s > R(0) ? R(2) * vx_atan2(s, qw) / s : R(0);
+  const V3<R> th = to_bond<AX>(mk(k * qx, k * qy, k * qz));
+
+  // Eq. 40: X2 = d_x - L_T with L_T = l (1 + alpha_mean dT)
+  const R X2 = dv.x - l * c.alpha_mean * dT;
+  const R Y2 = dv.y, Z2 = dv.z;
+  const V3<R> fa = mk(c.a1 * X2, c.b1 * Y2 - c.b2 * th.z, c.b1 * Z2 + c.b2 * th.y);
+  const V3<R> ma = mk(c.a2 * th.x, -c.b2 * Z2 - c.b3 * th.y, c.b2 * Y2 - c.b3 * th.z);
+  const V3<R> mbl = mk(-c.a2 * th.x, -c.b2 * Z2 - R(2) * c.b3 * th.y,
+                       c.b2 * Y2 - R(2) * c.b3 * th.z);
+  V3<R> Fa = mul(Ra, to_world<AX>(fa));
+  V3<R> Ma = mul(Ra, to_world<AX>(ma));
+  V3<R> Mbw = mul(Ra, to_world<AX>(mbl));
+
+  // Eq. 33-35 in the world frame
+  const V3<R> Vb = Mb.inv_m * mk(mob.x, mob.y, mob.z);
+  const V3<R> wb = Mb.inv_I * mk(mob.w, anb.x, anb.y);
+  const V3<R> Vavg = R(0.5) * (Va + Vb);
+  const V3<R> wavg = R(0.5) * (wa + wb);
+  V3<R> r = du;
+  if constexpr (AX == 0) r.x += l;
+  else if constexpr (AX == 1) r.y += l;
+  else r.z += l;
+  const V3<R> Vr = (Vb - Vavg) + cross(R(0.5) * r, wavg);
+  const V3<R> wr = wb - wavg;
+  Fa = Fa + c.ct * Vr;
+  Ma = Ma + c.cr * wr;
+  Mbw = Mbw - c.cr * wr;
+
+  const size_t o = (size_t)AX * d.nloc + ia;
+  d.recA[o] = R4{Fa.x, Fa.y, Fa.z, Ma.x};
+  d.recB[o] = R4{Ma.y, Ma.z, Mbw.x, Mbw.y};
+  d.recC[o] = Mbw.z;
+  if (!(R(1) + c.alpha_mean * dT > R(0))) d.clk->fault = 1;
+}
+
+template <class R>
+__global__ void __launch_bounds__(256) k_bonds(Dev<R> d, uint32_t beg, uint32_t end) {
+  using R4 = typename VT<R>::R4;
+  using R2 = typename VT<R>::R2;
+  const uint32_t id = beg + blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= end) return;
+  const R4 pa = d.pos[id];
+  const uint32_t meta = meta_of(pa.w);
+  const uint32_t want = meta & (nb_bit(1) | nb_bit(3) | nb_bit(5));
+  if (!want) return;
+  const R4 qa = d.quat[id];
+  const R4 moa = d.mom[id];
+  const R2 ana = d.ang[id];
+  const int mat_a = meta & M_MAT;
+  const MatC<R>& Ma = d.mat[mat_a];
+  const Rot<R> Ra = rotation(qa.w, qa.x, qa.y, qa.z);
+  const V3<R> ua = mk(pa.x, pa.y, pa.z);
+  const V3<R> Va = Ma.inv_m * mk(moa.x, moa.y, moa.z);
+  const V3<R> wa = Ma.inv_I * mk(moa.w, ana.x, ana.y);
+  const R dT = (R)d.clk->dT;
+  if (want & nb_bit(1)) bond_one<0>(d, id, id + d.sx, Ra, qa, ua, Va, wa, mat_a, dT);
+  if (want & nb_bit(3)) bond_one<1>(d, id, id + d.nz, Ra, qa, ua, Va, wa, mat_a, dT);
+  if (want & nb_bit(5)) bond_one<2>(d, id, id + 1, Ra, qa, ua, Va, wa, mat_a, dT);
+}
+
+// ------------------------------------------------------------------ K4 integrate
+template <class R, bool COLLIDE>
+__global__ void __launch_bounds__(256) k_integrate(Dev<R> d, uint32_t beg, uint32_t end,
+                                                   const uint32_t* __restrict__ ext_of_local) {
+  using R4 = typename VT<R>::R4;
+  using R2 = typename VT<R>::R2;
+  const uint32_t id = beg + blockIdx.x * blockDim.x + threadIdx.x;
+  R vmax = R(0);
+  if (id < end) {
+    const R4 p = d.pos[id];
+    const uint32_t meta = meta_of(p.w);
+    if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
+      const MatC<R> mc = d.mat[meta & M_MAT];
+      const R4 mo = d.mom[id];
+      const R2 an = d.ang[id];
+      V3<R> F = mk(R(0), R(0), R(0)), M = F;
+      const uint32_t strides[3] = {d.sx, d.nz, 1u};
+      // Eq. 25-26 in slot order -x,+x,-y,+y,-z,+z: a -axis slot holds the
+      // bond (v-e, v) where v is "b" (-F_a, M_b); a +axis slot (F_a, M_a).
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (meta & nb_bit(2 * ax)) {
+          const size_t o = (size_t)ax * d.nloc + (id - strides[ax]);
+          const R4 A = d.recA[o];
+          const R4 B = d.recB[o];
+          const R C = d.recC[o];
+          F = F - mk(A.x, A.y, A.z);
+          M = M + mk(B.z, B.w, C);
+        }
+        if (meta & nb_bit(2 * ax + 1)) {
+          const size_t o = (size_t)ax * d.nloc + id;
+          const R4 A = d.recA[o];
+          const R4 B = d.recB[o];
+          F = F + mk(A.x, A.y, A.z);
+          M = M + mk(A.w, B.x, B.y);
+        }
+      }
+      if (meta & M_EXT) {
+        const R4 fe = d.fext[id];
+        F = F + mk(fe.x, fe.y, fe.z);
+      }
+      F.z = F.z - mc.mg;
+      const V3<R> V = mc.inv_m * mk(mo.x, mo.y, mo.z);
+      const V3<R> w = mc.inv_I * mk(mo.w, an.x, an.y);
+      if (d.ground) {                                     // P:254, R12
+        F = F - mc.cgt * V;
+        M = M - mc.cgr * w;
+      }
+      if constexpr (COLLIDE) {
+        if (meta & M_SURF) {
+          const R4 c = d.cf[id];
+          F = F + mk(c.x, c.y, c.z);
+        }
+      }
+      bool latch = (meta & M_LATCH) != 0;
+      bool zero_lat = false;
+      if (d.floor_on) {                                   // P:260-274, R14, R15
+        const R dT = (R)d.clk->dT;
+        const uint32_t kz = id % d.nz;
+        // penetration r_v - (D_z - z_floor), r_v = (l/2)(1 + alpha dT)
+        const R base = (R)(d.zbase_d + d.l_d * (double)kz);
+        const R pen = d.half_l * mc.alpha * dT - p.z - base;
+        if (pen > R(0)) {
+          R Fn = mc.kf * pen - mc.cfl * V.z;
+          if (Fn < R(0)) Fn = R(0);
+          F.z = F.z + Fn;
+          const R Flx = F.x, Fly = F.y;
+          const R Fl = vx_sqrt(Flx * Flx + Fly * Fly);
+          const R Vl = vx_sqrt(V.x * V.x + V.y * V.y);
+          if (latch) {
+            if (Fl <= mc.mu_s * Fn) {                     // Eq. 36 holds
+              F.x = R(0); F.y = R(0); zero_lat = true;
+            } else {                                      // break away, Eq. 37
+              latch = false;
+              F.x = Flx - mc.mu_d * Fn * Flx / Fl;
+              F.y = Fly - mc.mu_d * Fn * Fly / Fl;
+            }
+          } else {
+            if (Vl <= mc.mu_d * Fn * mc.dt_m) {           // Eq. 38 halt
+              F.x = R(0); F.y = R(0); zero_lat = true; latch = true;
+            } else {
+              F.x = Flx - mc.mu_d * Fn * V.x / Vl;
+              F.y = Fly - mc.mu_d * Fn * V.y / Vl;
+            }
+          }
+        } else {
+          latch = false;
+        }
+      }
+      // Eq. 27-30
+      V3<R> P = mk(mo.x, mo.y, mo.z) + d.dt * F;
+      if (zero_lat) { P.x = R(0); P.y = R(0); }
+      const V3<R> u = mk(p.x, p.y, p.z) + mc.dt_m * P;
+      const V3<R> phi = mk(mo.w, an.x, an.y) + d.dt * M;
+      const V3<R> th = mc.dt_I * phi;
+      const R a = vx_sqrt(dot(th, th));
+      R dw = R(1), dx = R(0), dy = R(0), dz = R(0);
+      if (a > R(0)) {
+        R sh, ch;
+        vx_sincos(R(0.5) * a, &sh, &ch);
+        const R sa = sh / a;
+        dw = ch; dx = sa * th.x; dy = sa * th.y; dz = sa * th.z;
+      }
+      const R4 q = d.quat[id];
+      R qw = dw * q.w - dx * q.x - dy * q.y - dz * q.z;
+      R qx = dw * q.x + dx * q.w + dy * q.z - dz * q.y;
+      R qy = dw * q.y - dx * q.z + dy * q.w + dz * q.x;
+      R qz = dw * q.z + dx * q.y - dy * q.x + dz * q.w;
+      const R qn = vx_sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+      qw = qw / qn; qx = qx / qn; qy = qy / qn; qz = qz / qn;
+      const uint32_t nmeta = latch ? (meta | M_LATCH) : (meta & ~M_LATCH);
+      d.pos[id] = R4{u.x, u.y, u.z, meta_as(R(0), nmeta)};
+      d.quat[id] = R4{qx, qy, qz, qw};
+      d.mom[id] = R4{P.x, P.y, P.z, phi.x};
+      d.ang[id] = R2{phi.y, phi.z};
+      const bool ok = vx_finite(u.x) && vx_finite(u.y) && vx_finite(u.z) && vx_finite(qw) &&
+                      vx_finite(qx) && vx_finite(qy) && vx_finite(qz) && vx_finite(P.x) &&
+                      vx_finite(P.y) && vx_finite(P.z) && vx_finite(phi.x) &&
+                      vx_finite(phi.y) && vx_finite(phi.z);
+      if (!ok) {
+        const unsigned long long code =
+            ((unsigned long long)d.clk->step << 32) | (unsigned long long)ext_of_local[id];
+        atomicMin(&d.clk->err, code);
+      }
+      if constexpr (COLLIDE) vmax = vx_sqrt(dot(P, P)) * mc.inv_m;
+    }
+  }
+  if constexpr (COLLIDE) {   // block max of |V| -> motion budget
+    __shared__ R sm[8];
+    R v = vmax;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) sm[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      v = lane < (int)(blockDim.x >> 5) ? sm[lane] : R(0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0 && v > R(0)) {
+        using UB = typename VT<R>::UB;
+        atomicMax((UB*)&d.clk->vmax_bits, (UB)rbits(v));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K5 broadphase
+// One CTA (1024 threads), gated by clk->rebuild.  Surface voxels are hashed
+// by cell floor(D / h), h >= cutoff; every pair with |D_a - D_b| < cutoff and
+// lattice Manhattan distance > 3 goes into a both-direction CSR whose
+// rows are sorted by partner id (deterministic).
+struct BroadArgs {
+  const int* surf;    // S local ids, ascending
+  int S;
+  int4* cellh;        // per surface voxel: cell x,y,z and hash
+  int* bcount;        // H
+  int* bstart;        // H + 1
+  int* bitems;        // S
+  int* rowptr;        // S + 1
+  int* col;           // cap
+  long long cap;
+  int H;              // power of two
+  Clock* clk;
+};
+
+__device__ __forceinline__ int cell_hash(int x, int y, int z, int H) {
+  unsigned h = (unsigned)x * 73856093u ^ (unsigned)y * 19349663u ^ (unsigned)z * 83492791u;
+  return (int)(h & (unsigned)(H - 1));
+}
+
+// In-place exclusive scan of a[0..n) by one CTA of 1024 threads; a[n] = total.
+__device__ void cta_exscan(int* a, int n) {
+  __shared__ int part[1024];
+  const int T = blockDim.x, t = threadIdx.x;
+  const int chunk = (n + T - 1) / T;
+  const int b = min(n, t * chunk), e = min(n, b + chunk);
+  int s = 0;
+  for (int i = b; i < e; ++i) s += a[i];
+  part[t] = s;
+  __syncthreads();
+  for (int off = 1; off < T; off <<= 1) {
+    int v = t >= off ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int run = part[t] - s;
+  for (int i = b; i < e; ++i) {
+    int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  if (t == T - 1) a[n] = part[T - 1];
+  __syncthreads();
+}
+
+template <class R>
+__device__ __forceinline__ void surf_geom(const Dev<R>& d, int id, int& i, int& j, int& k) {
+  k = id % (int)d.nz;
+  j = (id / (int)d.nz) % (int)d.ny;
+  i = id / (int)(d.nz * d.ny) + d.xl0;
+}
+
+template <class R>
+__global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, double ox,
+                                                     double oy, double oz, R h, R cutoff2) {
+  if (!d.clk->rebuild) return;
+  const int T = blockDim.x, t = threadIdx.x;
+  for (int x = t; x < b.H; x += T) b.bcount[x] = 0;
+  __syncthreads();
+  for (int s = t; s < b.S; s += T) {
+    const int id = b.surf[s];
+    int i, j, k;
+    surf_geom(d, id, i, j, k);
+    const typename VT<R>::R4 p = d.pos[id];
+    const R Dx = (R)(ox + d.l_d * ((double)i + 0.5)) + p.x;
+    const R Dy = (R)(oy + d.l_d * ((double)j + 0.5)) + p.y;
+    const R Dz = (R)(oz + d.l_d * ((double)k + 0.5)) + p.z;
+    const int cx = (int)floor(Dx / h), cy = (int)floor(Dy / h), cz = (int)floor(Dz / h);
+    const int hh = cell_hash(cx, cy, cz, b.H);
+    b.cellh[s] = make_int4(cx, cy, cz, hh);
+    atomicAdd(&b.bcount[hh], 1);
+  }
+  __syncthreads();
+  for (int x = t; x < b.H; x += T) b.bstart[x] = b.bcount[x];
+  __syncthreads();
+  cta_exscan(b.bstart, b.H);
+  for (int x = t; x < b.H; x += T) b.bcount[x] = 0;
+  __syncthreads();
+  for (int s = t; s < b.S; s += T) {
+    const int hh = b.cellh[s].w;
+    b.bitems[b.bstart[hh] + atomicAdd(&b.bcount[hh], 1)] = s;
+  }
+  __syncthreads();
+  // two passes: count, then fill (pass 1 writes rowptr, pass 2 col)
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int s = t; s < b.S; s += T) {
+      const int4 cs = b.cellh[s];
+      const int ida = b.surf[s];
+      int ia, ja, ka;
+      surf_geom(d, ida, ia, ja, ka);
+      const typename VT<R>::R4 pa = d.pos[ida];
+      int cnt = 0;
+      const int base = pass ? b.rowptr[s] : 0;
+      for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int cx = cs.x + dx, cy = cs.y + dy, cz = cs.z + dz;
+            const int hh = cell_hash(cx, cy, cz, b.H);
+            for (int q = b.bstart[hh]; q < b.bstart[hh + 1]; ++q) {
+              const int u = b.bitems[q];
+              const int4 cu = b.cellh[u];
+              if (u == s || cu.x != cx || cu.y != cy || cu.z != cz) continue;
+              const int idb = b.surf[u];
+              int ib, jb, kb;
+              surf_geom(d, idb, ib, jb, kb);
+              if (abs(ia - ib) + abs(ja - jb) + abs(ka - kb) <= 3) continue;
+              const typename VT<R>::R4 pb = d.pos[idb];
+              const R rx = d.l * (R)(ia - ib) + (pa.x - pb.x);
+              const R ry = d.l * (R)(ja - jb) + (pa.y - pb.y);
+              const R rz = d.l * (R)(ka - kb) + (pa.z - pb.z);
+              if (rx * rx + ry * ry + rz * rz >= cutoff2) continue;
+              if (pass) {
+                if (base + cnt < b.cap) b.col[base + cnt] = idb;
+              }
+              ++cnt;
+            }
+          }
+      if (!pass) {
+        b.rowptr[s] = cnt;
+      } else if (base + cnt <= b.cap) {   // sort the row by partner id
+        for (int x = base + 1; x < base + cnt; ++x) {
+          const int v = b.col[x];
+          int y = x - 1;
+          while (y >= base && b.col[y] > v) { b.col[y + 1] = b.col[y]; --y; }
+          b.col[y + 1] = v;
+        }
+      }
+    }
+    __syncthreads();
+    if (!pass) {
+      cta_exscan(b.rowptr, b.S);
+      if (t == 0) {
+        const long long tot = b.rowptr[b.S];
+        if (tot > b.cap) d.clk->overflow = 1;
+        d.clk->npairs = tot / 2;
+        d.clk->rebuilds += 1;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------------ contact
+// Penalty law of reading R16: F_on_a = max(0, k_c q - c_c v_n) n,
+// q = r_a + r_b - |D_a - D_b|; partners summed in ascending id.
+template <class R>
+__global__ void __launch_bounds__(256) k_contact(Dev<R> d, const int* surf, int S,
+                                                 const int* rowptr, const int* col,
+                                                 R zeta_col) {
+  using R4 = typename VT<R>::R4;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const int ida = surf[s];
+  int ia, ja, ka;
+  surf_geom(d, ida, ia, ja, ka);
+  const R4 pa = d.pos[ida];
+  const int mat_a = meta_of(pa.w) & M_MAT;
+  const MatC<R>& ma = d.mat[mat_a];
+  const R4 moa = d.mom[ida];
+  const R dT = (R)d.clk->dT;
+  const R ra = d.half_l * (R(1) + ma.alpha * dT);
+  V3<R> F = mk(R(0), R(0), R(0));
+  for (int q = rowptr[s]; q < rowptr[s + 1]; ++q) {
+    const int idb = col[q];
+    int ib, jb, kb;
+    surf_geom(d, idb, ib, jb, kb);
+    const R4 pb = d.pos[idb];
+    const int mat_b = meta_of(pb.w) & M_MAT;
+    const MatC<R>& mb = d.mat[mat_b];
+    const R rb = d.half_l * (R(1) + mb.alpha * dT);
+    const V3<R> dd = mk(d.l * (R)(ia - ib) + (pa.x - pb.x), d.l * (R)(ja - jb) + (pa.y - pb.y),
+                        d.l * (R)(ka - kb) + (pa.z - pb.z));
+    const R dist = vx_sqrt(dot(dd, dd));
+    const R pen = ra + rb - dist;
+    if (!(pen > R(0))) continue;
+    V3<R> n;
+    if (dist > R(0)) n = (R(1) / dist) * dd;
+    else n = mk(R(0), R(0), ida < idb ? R(1) : R(-1));
+    const R4 mob = d.mom[idb];
+    const V3<R> Va = ma.inv_m * mk(moa.x, moa.y, moa.z);
+    const V3<R> Vb = mb.inv_m * mk(mob.x, mob.y, mob.z);
+    const R vn = dot(Va - Vb, n);
+    const R kc = R(2) * ma.kc * mb.kc / (ma.kc + mb.kc);
+    const R cc = R(2) * zeta_col * vx_sqrt(fmin(ma.m, mb.m) * kc);
+    R f = kc * pen - cc * vn;
+    if (f < R(0)) f = R(0);
+    F = F + f * n;
+  }
+  d.cf[ida] = R4{F.x, F.y, F.z, R(0)};
+}
+
+// ------------------------------------------------------------------ state I/O
+// Rest site coordinate o + l (i + 1/2), rounded as two separate fp64
+// operations (no FMA contraction), i.e. exactly as a caller forms it.
+__device__ __forceinline__ double site(double o, double l, long long i) {
+  return __dadd_rn(o, __dmul_rn(l, (double)i + 0.5));
+}
+
+// External arrays (fp64) <-> device state.  box_of_ext[e] = global box id of
+// external voxel e; local id = box - box_base when within [0, nloc).
+template <class R>
+__global__ void k_scatter_state(Dev<R> d, const long long* box_of_ext, long long N,
+                                long long box_base, const double* pos, const double* quat,
+                                const double* lin, const double* ang, const uint8_t* latch,
+                                double ox, double oy, double oz) {
+  using R4 = typename VT<R>::R4;
+  using R2 = typename VT<R>::R2;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N) return;
+  const long long g = box_of_ext[e];
+  const long long li = g - box_base;
+  if (li < 0 || li >= (long long)d.nloc) return;
+  const long long nyz = (long long)d.ny * d.nz;
+  const long long i = g / nyz, j = (g / d.nz) % d.ny, k = g % d.nz;
+  const double l = d.l_d;
+  R4 p = d.pos[li];
+  if (pos) {
+    p.x = (R)(pos[3 * e] - site(ox, l, i));
+    p.y = (R)(pos[3 * e + 1] - site(oy, l, j));
+    p.z = (R)(pos[3 * e + 2] - site(oz, l, k));
+  }
+  if (latch) {
+    uint32_t m = meta_of(p.w);
+    m = latch[e] ? (m | M_LATCH) : (m & ~M_LATCH);
+    p.w = meta_as(R(0), m);
+  }
+  d.pos[li] = p;
+  if (quat) d.quat[li] = R4{(R)quat[4 * e + 1], (R)quat[4 * e + 2], (R)quat[4 * e + 3], (R)quat[4 * e]};
+  R4 mo = d.mom[li];
+  R2 an = d.ang[li];
+  if (lin) { mo.x = (R)lin[3 * e]; mo.y = (R)lin[3 * e + 1]; mo.z = (R)lin[3 * e + 2]; }
+  if (ang) { mo.w = (R)ang[3 * e]; an.x = (R)ang[3 * e + 1]; an.y = (R)ang[3 * e + 2]; }
+  d.mom[li] = mo;
+  d.ang[li] = an;
+}
+
+// Owned local range -> box-ordered fp64 SoA (14 components x nbox_global).
+template <class R>
+__global__ void k_pack_box(Dev<R> d, uint32_t beg, uint32_t end, long long box_base,
+                           long long nbox, double* out, double ox, double oy, double oz) {
+  const uint32_t li = beg + blockIdx.x * blockDim.x + threadIdx.x;
+  if (li >= end) return;
+  const long long g = box_base + li;
+  const long long nyz = (long long)d.ny * d.nz;
+  const long long i = g / nyz, j = (g / d.nz) % d.ny, k = g % d.nz;
+  const double l = d.l_d;
+  const auto p = d.pos[li];
+  const auto q = d.quat[li];
+  const auto mo = d.mom[li];
+  const auto an = d.ang[li];
+  double v[14] = {site(ox, l, i) + (double)p.x, site(oy, l, j) + (double)p.y,
+                  site(oz, l, k) + (double)p.z, (double)q.w, (double)q.x,
+                  (double)q.y, (double)q.z, (double)mo.x, (double)mo.y, (double)mo.z,
+                  (double)mo.w, (double)an.x, (double)an.y,
+                  (meta_of(p.w) & M_LATCH) ? 1.0 : 0.0};
+#pragma unroll
+  for (int c = 0; c < 14; ++c) out[c * nbox + g] = v[c];
+}
+
+// box-ordered SoA -> external-order arrays
+__global__ void k_box_to_ext(const double* box, long long nbox, const long long* box_of_ext,
+                             long long N, double* pos, double* quat, double* lin, double* ang,
+                             uint8_t* latch) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N) return;
+  const long long g = box_of_ext[e];
+  for (int c = 0; c < 3; ++c) pos[3 * e + c] = box[c * nbox + g];
+  for (int c = 0; c < 4; ++c) quat[4 * e + c] = box[(3 + c) * nbox + g];
+  for (int c = 0; c < 3; ++c) lin[3 * e + c] = box[(7 + c) * nbox + g];
+  for (int c = 0; c < 3; ++c) ang[3 * e + c] = box[(10 + c) * nbox + g];
+  latch[e] = box[13 * nbox + g] != 0.0;
+}
+
+// Selected voxels (local ids, -1 = not owned) -> fp64 arrays.
+template <class R>
+__global__ void k_read_ids(Dev<R> d, const long long* lids, const long long* gids, long long n,
+                           double* pos, double* quat, double* lin, double* ang,
+                           uint8_t* latch, double ox, double oy, double oz) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const long long li = lids[e], g = gids[e];
+  const long long nyz = (long long)d.ny * d.nz;
+  const long long i = g / nyz, j = (g / d.nz) % d.ny, k = g % d.nz;
+  const double l = d.l_d;
+  const auto p = d.pos[li];
+  const auto q = d.quat[li];
+  const auto mo = d.mom[li];
+  const auto an = d.ang[li];
+  pos[3 * e] = site(ox, l, i) + (double)p.x;
+  pos[3 * e + 1] = site(oy, l, j) + (double)p.y;
+  pos[3 * e + 2] = site(oz, l, k) + (double)p.z;
+  quat[4 * e] = q.w; quat[4 * e + 1] = q.x; quat[4 * e + 2] = q.y; quat[4 * e + 3] = q.z;
+  lin[3 * e] = mo.x; lin[3 * e + 1] = mo.y; lin[3 * e + 2] = mo.z;
+  ang[3 * e] = mo.w; ang[3 * e + 1] = an.x; ang[3 * e + 2] = an.y;
+  latch[e] = (meta_of(p.w) & M_LATCH) ? 1 : 0;
+}
+
+// Merge static meta bits (material, filled, fixed, surface, ext, neighbours)
+// with the dynamic latch bit.
+template <class R>
+__global__ void k_merge_meta(Dev<R> d, const uint32_t* meta_static, uint32_t n) {
+  const uint32_t li = blockIdx.x * blockDim.x + threadIdx.x;
+  if (li >= n) return;
+  auto p = d.pos[li];
+  const uint32_t m = (meta_static[li] & ~M_LATCH) | (meta_of(p.w) & M_LATCH);
+  p.w = meta_as(decltype(p.x)(0), m);
+  d.pos[li] = p;
+}
+
+}  // namespace vx

@@ -1,0 +1,227 @@
+"""Thin Python binding of the C ABI (include/voxsim.h): same names, argument
+marshalling only -- every step of the path runs in libvoxsim.so's kernels."""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+
+class VoxError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"[{status}] {msg}")
+        self.status = status
+
+
+class DivergedError(VoxError):
+    pass
+
+
+class NoDeviceError(VoxError):
+    pass
+
+
+def _check(status):
+    if status != N.VX_OK:
+        msg = N.load().vx_last_error().decode()
+        cls = {N.VX_ERR_DIVERGED: DivergedError, N.VX_ERR_NO_DEVICE: NoDeviceError}.get(status, VoxError)
+        raise cls(status, msg)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+@dataclass
+class State:
+    pos: np.ndarray      # (n,3) absolute positions D, m
+    quat: np.ndarray     # (n,4) w,x,y,z
+    linmom: np.ndarray   # (n,3) P
+    angmom: np.ndarray   # (n,3) phi
+    latch: np.ndarray    # (n,) uint8
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(N.load().vx_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Lattice:
+    """One voxel lattice on one GPU (one x-slab of it when nranks > 1)."""
+
+    def __init__(self, handle, n):
+        self._h = handle
+        self.n = n
+
+    # ------------------------------------------------------------ vx_create_lattice
+    @classmethod
+    def create_lattice(cls, cells, lattice_dim, origin=(0.0, 0.0, 0.0), precision=32, device=0,
+                       rank=0, nranks=1, nccl_id=None):
+        """cells: uint8 array of shape (nz, ny, nx) (flat order x-fastest)."""
+        L = N.load()
+        cells = np.ascontiguousarray(cells, dtype=np.uint8)
+        nz, ny, nx = cells.shape
+        d = N.vx_lattice_desc()
+        d.nx, d.ny, d.nz = nx, ny, nz
+        d.lattice_dim = float(lattice_dim)
+        d.origin = (ctypes.c_double * 3)(*[float(x) for x in origin])
+        d.cells = cells.ctypes.data
+        d.precision = int(precision)
+        d.device, d.rank, d.nranks = int(device), int(rank), int(nranks)
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            d.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
+        h = ctypes.c_void_p()
+        _check(L.vx_create_lattice(ctypes.byref(d), ctypes.byref(h)))
+        return cls(h, int(L.vx_num_voxels(h)))
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            N.load().vx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ setup
+    def set_materials(self, materials):
+        arr = (N.vx_material * len(materials))()
+        for i, m in enumerate(materials):
+            arr[i] = N.vx_material(m["E"], m["nu"], m["rho"], m.get("cte", 0.0),
+                                   m.get("mu_s", 0.0), m.get("mu_d", 0.0))
+        _check(N.load().vx_set_materials(self._h, arr, len(materials)))
+
+    def set_environment(self, env):
+        e = N.vx_env(env.get("gravity", 0.0), int(env.get("floor_on", 0)),
+                     env.get("floor_z", 0.0), env.get("T_ref", 0.0), env.get("T_amp", 0.0),
+                     env.get("T_freq", 0.0), env.get("T_phase", 0.0),
+                     env.get("zeta_bond", 0.0), env.get("zeta_ground", 0.0),
+                     env.get("zeta_col", 0.0), env.get("horizon_voxels", 2.0),
+                     env.get("dt_safety", 1.0), int(env.get("self_collision", 0)))
+        _check(N.load().vx_set_environment(self._h, ctypes.byref(e)))
+
+    def set_boundary(self, fixed=None, f_ext=None):
+        f = None if fixed is None else np.ascontiguousarray(fixed, dtype=np.uint8)
+        x = None if f_ext is None else np.ascontiguousarray(f_ext, dtype=np.float64)
+        _check(N.load().vx_set_boundary(self._h, _ptr(f), _ptr(x)))
+
+    def add_region(self, kind, origin, size, force=(0.0, 0.0, 0.0)):
+        k = {"fixed": 0, "forced": 1}.get(kind, kind)
+        o = (ctypes.c_double * 3)(*map(float, origin))
+        s = (ctypes.c_double * 3)(*map(float, size))
+        f = (ctypes.c_double * 3)(*map(float, force))
+        _check(N.load().vx_add_region(self._h, int(k), o, s, f))
+
+    def set_state(self, pos=None, quat=None, linmom=None, angmom=None, latch=None):
+        arrs = [None if a is None else np.ascontiguousarray(a, dtype=t)
+                for a, t in ((pos, np.float64), (quat, np.float64), (linmom, np.float64),
+                             (angmom, np.float64), (latch, np.uint8))]
+        _check(N.load().vx_set_state(self._h, *[_ptr(a) for a in arrs]))
+
+    def set_step(self, n):
+        _check(N.load().vx_set_step(self._h, int(n)))
+
+    # ------------------------------------------------------------ stepping
+    def step(self, n=1):
+        _check(N.load().vx_step(self._h, int(n)))
+
+    def read_state(self, out: State | None = None) -> State:
+        n = self.n
+        if out is None:
+            out = State(np.empty((n, 3)), np.empty((n, 4)), np.empty((n, 3)), np.empty((n, 3)),
+                        np.empty(n, np.uint8))
+        _check(N.load().vx_read_state(self._h, _ptr(out.pos), _ptr(out.quat), _ptr(out.linmom),
+                                      _ptr(out.angmom), _ptr(out.latch)))
+        return out
+
+    def read_voxels(self, ids) -> State:
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        n = len(ids)
+        out = State(np.empty((n, 3)), np.empty((n, 4)), np.empty((n, 3)), np.empty((n, 3)),
+                    np.empty(n, np.uint8))
+        _check(N.load().vx_read_voxels(self._h, _ptr(ids), n, _ptr(out.pos), _ptr(out.quat),
+                                       _ptr(out.linmom), _ptr(out.angmom), _ptr(out.latch)))
+        return out
+
+    # ------------------------------------------------------------ queries
+    @property
+    def dt(self):
+        return N.load().vx_dt(self._h)
+
+    @property
+    def num_voxels(self):
+        return int(N.load().vx_num_voxels(self._h))
+
+    @property
+    def num_bonds(self):
+        return int(N.load().vx_num_bonds(self._h))
+
+    @property
+    def num_surface(self):
+        return int(N.load().vx_num_surface(self._h))
+
+    @property
+    def steps_done(self):
+        return int(N.load().vx_steps_done(self._h))
+
+    @property
+    def num_contact_pairs(self):
+        return int(N.load().vx_num_contact_pairs(self._h))
+
+    @property
+    def num_rebuilds(self):
+        return int(N.load().vx_num_rebuilds(self._h))
+
+    def owned_planes(self):
+        a, b = ctypes.c_int32(), ctypes.c_int32()
+        N.load().vx_owned_planes(self._h, ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value
+
+    @property
+    def stream(self) -> int:
+        """cudaStream_t of the library (wrap with torch.cuda.ExternalStream)."""
+        return int(N.load().vx_stream(self._h) or 0)
+
+    def set_instrumentation(self, on=True):
+        _check(N.load().vx_set_instrumentation(self._h, int(bool(on))))
+
+    def kernel_times(self):
+        ms = (ctypes.c_double * 4)()
+        cnt = (ctypes.c_int64 * 4)()
+        _check(N.load().vx_kernel_times(self._h, ms, cnt))
+        names = ("bonds", "integrate", "other", "all")
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(names)}
+
+    @property
+    def launches_per_step(self):
+        return int(N.load().vx_launches_per_step(self._h))
+
+
+def create_lattice(*a, **kw) -> Lattice:
+    return Lattice.create_lattice(*a, **kw)
+
+
+def from_scene(scene, precision=None, device=0, rank=0, nranks=1, nccl_id=None,
+               init_state=True) -> Lattice:
+    """Convenience: a Lattice set up from a workloads.Scene (no arithmetic).
+    ``init_state=False`` keeps the library's initial state (at rest on the
+    lattice sites), which equals the scene's when it has no v0."""
+    lat = Lattice.create_lattice(scene.cells, scene.lattice_dim, scene.origin,
+                                 precision or scene.precision, device, rank, nranks, nccl_id)
+    lat.set_materials(scene.materials)
+    lat.set_environment(scene.env)
+    if scene.fixed is not None or scene.fext is not None:
+        lat.set_boundary(scene.fixed, scene.fext)
+    for kind, org, size, force in scene.extra.get("regions", []):
+        lat.add_region(kind, org, size, force)
+    if init_state:
+        lat.set_state(*scene.initial_state())
+    return lat
