@@ -131,6 +131,17 @@ vx_status vx_add_region(vx_lattice* h, int32_t kind, const double origin[3],
 vx_status vx_set_state(vx_lattice* h, const double* pos, const double* quat,
                        const double* linmom, const double* angmom, const uint8_t* latch);
 
+/* Exact checkpoint of this rank's device state (displacements, orientations,
+ * momenta, latch bits, step counter, motion budget), for bitwise resume:
+ * load(save(x)) then step(k) equals the uninterrupted run bit for bit.
+ * (vx_read_state / vx_set_state go through absolute fp64 positions and are
+ * exact only to rounding.)  The buffer is caller-owned host memory of
+ * vx_checkpoint_bytes() bytes; load checks the lattice shape and precision
+ * (INVALID_ARG on mismatch). */
+int64_t vx_checkpoint_bytes(const vx_lattice* h);
+vx_status vx_save_checkpoint(vx_lattice* h, void* buf, int64_t bytes);
+vx_status vx_load_checkpoint(vx_lattice* h, const void* buf, int64_t bytes);
+
 /* Set the step counter n (time t_n = n dt of the temperature schedule). */
 vx_status vx_set_step(vx_lattice* h, int64_t n);
 
@@ -164,6 +175,12 @@ int64_t vx_steps_done(const vx_lattice* h);        /* step counter n            
 int64_t vx_num_contact_pairs(const vx_lattice* h); /* current shortlist size (pairs a<b) */
 int64_t vx_num_rebuilds(const vx_lattice* h);      /* broadphase rebuilds so far     */
 int32_t vx_owned_planes(const vx_lattice* h, int32_t* x_begin, int32_t* x_end); /* this rank's x-slab */
+
+/* Copy the current collision shortlist as external-id pairs (a < b),
+ * ascending, into pairs[2*cap]; returns the total number of pairs (which may
+ * exceed cap), 0 when self collision is off, -1 on error.  The list holds
+ * every surface pair within the horizon cutoff at the last rebuild. */
+int64_t vx_contact_pairs(vx_lattice* h, int64_t* pairs, int64_t cap);
 
 /* The CUDA stream every kernel of this lattice is launched on (cudaStream_t).
  * Owned by the library; valid until vx_destroy. */

@@ -62,6 +62,9 @@ SIGNATURES = {
     "vx_add_region": (_I32, [_P, _I32, _DP, _DP, _DP]),
     "vx_set_state": (_I32, [_P, _P, _P, _P, _P, _P]),
     "vx_set_step": (_I32, [_P, _I64]),
+    "vx_checkpoint_bytes": (_I64, [_P]),
+    "vx_save_checkpoint": (_I32, [_P, _P, _I64]),
+    "vx_load_checkpoint": (_I32, [_P, _P, _I64]),
     "vx_step": (_I32, [_P, _I64]),
     "vx_read_state": (_I32, [_P, _P, _P, _P, _P, _P]),
     "vx_read_voxels": (_I32, [_P, _P, _I64, _P, _P, _P, _P, _P]),
@@ -74,6 +77,7 @@ SIGNATURES = {
     "vx_num_rebuilds": (_I64, [_P]),
     "vx_owned_planes": (_I32, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "vx_stream": (_P, [_P]),
+    "vx_contact_pairs": (_I64, [_P, _P, _I64]),
     "vx_set_instrumentation": (_I32, [_P, _I32]),
     "vx_kernel_times": (_I32, [_P, _DP, ctypes.POINTER(_I64)]),
     "vx_launches_per_step": (_I32, [_P]),

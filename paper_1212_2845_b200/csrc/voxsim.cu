@@ -834,6 +834,61 @@ vx_status vx_set_state(vx_lattice* h, const double* pos, const double* quat, con
   return VX_OK;
 }
 
+namespace {
+struct CkptHeader {
+  uint64_t magic;
+  int32_t prec, rank;
+  int64_t nloc, N, steps_done;
+};
+const uint64_t kCkptMagic = 0x31504b43584f56ULL;  // "VOXCKP1"
+}  // namespace
+
+int64_t vx_checkpoint_bytes(const vx_lattice* h) {
+  if (!h) return -1;
+  return (int64_t)(sizeof(CkptHeader) + h->pos.bytes + h->quat.bytes + h->mom.bytes +
+                   h->ang.bytes + sizeof(Clock));
+}
+
+vx_status vx_save_checkpoint(vx_lattice* h, void* buf, int64_t bytes) {
+  if (!h || !buf || bytes < vx_checkpoint_bytes(h)) return fail(VX_ERR_INVALID_ARG, "bad checkpoint buffer");
+  VX_TRY(set_device(h));
+  char* p = static_cast<char*>(buf);
+  CkptHeader hd{kCkptMagic, h->prec, h->rank, (int64_t)h->nloc, h->N, h->steps_done};
+  std::memcpy(p, &hd, sizeof hd);
+  p += sizeof hd;
+  for (DevBuf* b : {&h->pos, &h->quat, &h->mom, &h->ang, &h->clk}) {
+    VX_CUDA(cudaMemcpy(p, b->p, b->bytes, cudaMemcpyDeviceToHost));
+    p += b->bytes;
+  }
+  return VX_OK;
+}
+
+vx_status vx_load_checkpoint(vx_lattice* h, const void* buf, int64_t bytes) {
+  if (!h || !buf || bytes < vx_checkpoint_bytes(h)) return fail(VX_ERR_INVALID_ARG, "bad checkpoint buffer");
+  VX_TRY(set_device(h));
+  const char* p = static_cast<const char*>(buf);
+  CkptHeader hd;
+  std::memcpy(&hd, p, sizeof hd);
+  if (hd.magic != kCkptMagic || hd.prec != h->prec || hd.nloc != (int64_t)h->nloc || hd.N != h->N ||
+      hd.rank != h->rank)
+    return fail(VX_ERR_INVALID_ARG, "checkpoint does not match this lattice (shape, precision or rank)");
+  p += sizeof hd;
+  for (DevBuf* b : {&h->pos, &h->quat, &h->mom, &h->ang}) {
+    VX_CUDA(cudaMemcpy(b->p, p, b->bytes, cudaMemcpyHostToDevice));
+    p += b->bytes;
+  }
+  Clock c;
+  std::memcpy(&c, p, sizeof c);
+  c.force_rebuild = 1;   // the pair list is rebuilt from the restored state
+  c.err = ~0ULL;
+  c.fault = 0;
+  c.overflow = 0;
+  VX_CUDA(cudaMemcpy(h->clk.p, &c, sizeof c, cudaMemcpyHostToDevice));
+  h->steps_done = hd.steps_done;
+  // static meta bits follow this lattice's boundary conditions (latch kept)
+  return upload_meta(h);
+}
+
 vx_status vx_set_step(vx_lattice* h, int64_t n) {
   if (!h || n < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
   VX_TRY(set_device(h));
@@ -998,6 +1053,37 @@ int32_t vx_owned_planes(const vx_lattice* h, int32_t* xb, int32_t* xe) {
   return h->x1 - h->x0;
 }
 void* vx_stream(const vx_lattice* h) { return h ? (void*)h->stream : nullptr; }
+
+int64_t vx_contact_pairs(vx_lattice* h, int64_t* pairs, int64_t cap) {
+  if (!h) return -1;
+  if (!h->collide() || h->tables_dirty || !h->rowptr.p) return 0;
+  if (cudaSetDevice(h->device) != cudaSuccess) return -1;
+  const int S = (int)h->surf_local.size();
+  std::vector<int> rp(S + 1);
+  if (cudaMemcpy(rp.data(), h->rowptr.p, (size_t)(S + 1) * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  const long long tot = std::min<long long>(rp[S], h->cap);
+  std::vector<int> col((size_t)std::max<long long>(tot, 1));
+  if (tot && cudaMemcpy(col.data(), h->col.p, (size_t)tot * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  std::vector<long long> eol(h->nloc, -1);
+  for (long long e = 0; e < h->N; ++e) {
+    const long long li = h->box_of_ext[e] - h->box_base;
+    if (li >= 0 && li < (long long)h->nloc) eol[li] = e;
+  }
+  std::vector<std::pair<long long, long long>> out;
+  for (int s = 0; s < S; ++s) {
+    const long long a = eol[h->surf_local[s]];
+    for (int q = rp[s]; q < std::min<long long>(rp[s + 1], tot); ++q) {
+      const long long b = eol[col[q]];
+      if (a < b) out.emplace_back(a, b);
+    }
+  }
+  std::sort(out.begin(), out.end());
+  for (long long i = 0; i < (long long)out.size() && i < cap; ++i) {
+    pairs[2 * i] = out[i].first;
+    pairs[2 * i + 1] = out[i].second;
+  }
+  return (int64_t)out.size();
+}
 
 vx_status vx_set_instrumentation(vx_lattice* h, int32_t on) {
   if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");

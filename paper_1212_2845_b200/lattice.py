@@ -126,6 +126,17 @@ class Lattice:
                              (angmom, np.float64), (latch, np.uint8))]
         _check(N.load().vx_set_state(self._h, *[_ptr(a) for a in arrs]))
 
+    def save_checkpoint(self) -> bytes:
+        """Exact device-state snapshot (bitwise resume)."""
+        n = int(N.load().vx_checkpoint_bytes(self._h))
+        buf = ctypes.create_string_buffer(n)
+        _check(N.load().vx_save_checkpoint(self._h, buf, n))
+        return buf.raw
+
+    def load_checkpoint(self, blob: bytes):
+        buf = ctypes.create_string_buffer(bytes(blob), len(blob))
+        _check(N.load().vx_load_checkpoint(self._h, buf, len(blob)))
+
     def set_step(self, n):
         _check(N.load().vx_set_step(self._h, int(n)))
 
@@ -179,6 +190,14 @@ class Lattice:
     @property
     def num_rebuilds(self):
         return int(N.load().vx_num_rebuilds(self._h))
+
+    def contact_pairs(self, cap=1 << 22):
+        """Current collision shortlist as (n,2) external ids, a < b."""
+        buf = np.zeros(2 * cap, np.int64)
+        n = int(N.load().vx_contact_pairs(self._h, buf.ctypes.data, cap))
+        if n < 0:
+            raise VoxError(n, "vx_contact_pairs failed")
+        return buf[:2 * min(n, cap)].reshape(-1, 2)
 
     def owned_planes(self):
         a, b = ctypes.c_int32(), ctypes.c_int32()

@@ -1,0 +1,100 @@
+"""C5 scaling block at its full size (512x256x256, 33.5M voxels) in the launch
+configuration bench.py times (fp32, CUDA-graph chunks), checked on sampled
+voxels the oracle recomputes one by one.
+
+A voxel's update depends only on its own state, its six face neighbours' and
+the step's scalars (loads from the frozen state, then the update), so
+for each sample the oracle steps the 3x3x3 sub-lattice (centre + face
+neighbours, same materials, same origin offset, same dt and step index) from
+the GPU's state at step n and its centre is compared with the GPU at n+1."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import OracleSim
+from paper_1212_2845_b200 import from_scene
+
+pytestmark = pytest.mark.gpu
+
+NX, NY, NZ = 512, 256, 256
+
+
+def _ext(i, j, k):
+    return i + NX * (j + NY * k)
+
+
+def _samples(rng):
+    pts = set()
+    for i in (0, NX - 1):
+        for j in (0, NY - 1):
+            for k in (0, NZ - 1):
+                pts.add((i, j, k))                                   # corners
+    for _ in range(60):                                              # floor layer
+        pts.add((int(rng.integers(NX)), int(rng.integers(NY)), 0))
+    for _ in range(40):                                              # slab faces
+        pts.add((int(rng.choice([0, NX - 1])), int(rng.integers(NY)), int(rng.integers(NZ))))
+    for _ in range(40):                                              # material cell edges
+        pts.add((8 * int(rng.integers(1, NX // 8)) - 1, int(rng.integers(NY)),
+                 int(rng.integers(NZ))))
+    for _ in range(160):                                             # anywhere
+        pts.add((int(rng.integers(NX)), int(rng.integers(NY)), int(rng.integers(NZ))))
+    return sorted(pts)
+
+
+def test_c5_full_size_sampled_one_step():
+    sc = W.block(precision=32)
+    lat = from_scene(sc, precision=32, init_state=False)
+    assert lat.num_voxels == NX * NY * NZ
+    lat.step(3)        # bench warm-up
+    lat.step(20)       # graph chunks
+    n = lat.steps_done
+    rng = np.random.default_rng(7)
+    pts = _samples(rng)
+    offs = [(0, 0, 0), (-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)]
+    nb = {}
+    for (i, j, k) in pts:
+        for (a, b, c) in offs:
+            p = (i + a, j + b, k + c)
+            if 0 <= p[0] < NX and 0 <= p[1] < NY and 0 <= p[2] < NZ:
+                nb[p] = _ext(*p)
+    keys = sorted(nb)
+    before = lat.read_voxels([nb[p] for p in keys])
+    idx = {p: q for q, p in enumerate(keys)}
+    lat.step(1)
+    after = lat.read_voxels([_ext(*p) for p in pts])
+    cells_g = sc.cells
+    dP, dPo, dphi, dphio, dD, dDo = [], [], [], [], [], []
+    latch_ok = 0
+    for s, (i, j, k) in enumerate(pts):
+        sub = np.zeros((3, 3, 3), np.uint8)
+        members = []
+        for (a, b, c) in offs:
+            p = (i + a, j + b, k + c)
+            if p in idx:
+                sub[c + 1, b + 1, a + 1] = cells_g[p[2], p[1], p[0]]
+        kk, jj, ii = np.nonzero(sub)            # x-fastest order of the sub-grid
+        for (x, y, z) in zip(ii, jj, kk):
+            members.append((i + x - 1, j + y - 1, k + z - 1))
+        q = [idx[p] for p in members]
+        o = OracleSim(sub, sc.lattice_dim, sc.materials, sc.env,
+                      origin=((i - 1) * sc.lattice_dim, (j - 1) * sc.lattice_dim,
+                              (k - 1) * sc.lattice_dim))
+        o.set_dt(lat.dt)
+        o.set_step(n)
+        o.set_state(before.pos[q], before.quat[q], before.linmom[q], before.angmom[q],
+                    before.latch[q])
+        o.step(1)
+        r = o.read_state()
+        c = members.index((i, j, k))
+        b0 = idx[(i, j, k)]
+        dP.append(after.linmom[s] - before.linmom[b0]); dPo.append(r.linmom[c] - before.linmom[b0])
+        dphi.append(after.angmom[s] - before.angmom[b0]); dphio.append(r.angmom[c] - before.angmom[b0])
+        dD.append(after.pos[s] - before.pos[b0]); dDo.append(r.pos[c] - before.pos[b0])
+        latch_ok += int(after.latch[s] == r.latch[c])
+    dP, dPo, dphi, dphio, dD, dDo = map(np.array, (dP, dPo, dphi, dphio, dD, dDo))
+    eP = np.abs(dP - dPo).max() / np.abs(dPo).max()
+    ephi = np.abs(dphi - dphio).max() / max(np.abs(dphio).max(), 1e-300)
+    eD = np.abs(dD - dDo).max() / np.abs(dDo).max()
+    assert latch_ok == len(pts)
+    assert eP <= 1e-4 and eD <= 1e-4, (eP, eD)
+    assert ephi <= 1e-3, ephi

@@ -61,6 +61,16 @@ def test_small_sphere_self_contact_long(prec):
 
 
 @pytest.mark.parametrize("prec", [64, 32])
+def test_two_bodies_collide_and_separate(prec):
+    sc = W.two_bodies()
+    g, o, e = _check(sc, 300, prec, chunks=6)
+    # they collided (momenta reversed) and total momentum is conserved
+    i = sc.voxel_coords()[:, 0]
+    assert g.linmom[i < 3, 0].sum() < 0 < g.linmom[i >= 3, 0].sum()
+    assert abs(g.linmom[:, 0].sum()) <= 1e-6 * np.abs(g.linmom[:, 0]).sum()
+
+
+@pytest.mark.parametrize("prec", [64, 32])
 def test_c4_walker_100_steps(prec):
     _check(W.walker(), 100, prec)
 

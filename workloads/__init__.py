@@ -49,7 +49,7 @@ class Scene:
     origin: tuple = (0.0, 0.0, 0.0)
     fixed: np.ndarray | None = None   # (N,) uint8 in voxel-id order
     fext: np.ndarray | None = None    # (N,3) N
-    v0: np.ndarray | None = None      # (3,) initial velocity of every voxel, m/s
+    v0: np.ndarray | None = None      # (3,) or (N,3) initial velocities, m/s
     steps: int = 100                  # the config's step count
     precision: int = 64
     notes: str = ""
@@ -80,7 +80,8 @@ class Scene:
         if self.v0 is not None:
             mats = self.cells.ravel()[np.flatnonzero(self.cells.ravel())]
             rho = np.array([m["rho"] for m in self.materials])[mats - 1]
-            linmom = (rho * l ** 3)[:, None] * np.asarray(self.v0, np.float64)[None, :]
+            v0 = np.asarray(self.v0, np.float64)
+            linmom = (rho * l ** 3)[:, None] * (v0[None, :] if v0.ndim == 1 else v0)
         angmom = np.zeros((n, 3))
         latch = np.zeros(n, np.uint8)
         return pos, quat, linmom, angmom, latch
@@ -159,6 +160,23 @@ def block(nx=512, ny=256, nz=256, precision=32):
     name = "C5-block" if (nx, ny, nz) == (512, 256, 256) else f"C5-block-{nx}x{ny}x{nz}"
     return Scene(name, np.ascontiguousarray(cells), L, mats, env, steps=1000,
                  precision=precision, notes="resting on the floor")
+
+
+def two_bodies(n=3, gap=2, v=2.0, E=1e6):
+    """Two n^3 cubes, `gap` empty planes apart along x, approaching at +-v:
+    surface-voxel self collision between separate bodies."""
+    nx = 2 * n + gap
+    cells = np.zeros((n, n, nx), np.uint8)
+    cells[:, :, :n] = 1
+    cells[:, :, n + gap:] = 1
+    s = Scene("two-bodies", cells, L, [_mat(E, 1000.0)],
+              _env(zeta_bond=1.0, zeta_col=0.2, self_collision=1, horizon_voxels=2.0),
+              steps=300)
+    i = s.voxel_coords()[:, 0]
+    s.v0 = np.zeros((len(i), 3))
+    s.v0[i < n, 0] = v
+    s.v0[i >= n, 0] = -v
+    return s
 
 
 def app_a_beam():
