@@ -136,6 +136,25 @@ __global__ void __launch_bounds__(256) k_dt(const typename VT<R>::R4* pos, uint3
 }
 
 // ------------------------------------------------------------------ K3 bonds
+// Scale k with theta = k v for the unit quaternion (w >= 0, |v| = s):
+// k = 2 atan2(s, w) / s (reading R7).  Bond rotations are small (the beam
+// model's own range), so for s below a threshold the identity
+// 2 atan2(s, w) = 2 asin(s) (w = sqrt(1 - s^2)) is used through its series
+// 2 asin(s)/s = 2 (1 + s^2/6 + 3 s^4/40 + 5 s^6/112 + 35 s^8/1152), truncated
+// where the next term is below the type's rounding: no division, no atan2.
+template <class R> struct SeriesCut;
+template <> struct SeriesCut<float> { static constexpr float s2 = 0.125f * 0.125f; };
+template <> struct SeriesCut<double> { static constexpr double s2 = 0.002 * 0.002; };
+template <class R> __device__ __forceinline__ R rotvec_scale(R w, R x, R y, R z) {
+  const R s2 = x * x + y * y + z * z;
+  if (s2 < SeriesCut<R>::s2) {
+    return R(2) + s2 * (R(1) / R(3) + s2 * (R(3) / R(20) + s2 * (R(5) / R(56) +
+                                                          s2 * (R(35) / R(576)))));
+  }
+  const R s = vx_sqrt(s2);
+  return R(2) * vx_atan2(s, w) / s;
+}
+
 // Voxel a = id (negative side, R4), b = id + stride(AX).  Loads in the frame
 // of a, Eq. 13-24 sign-fixed and negated (R1, R3), back to world
 // (P:206), plus local damping (Eq. 33-35, R10, R11).
@@ -170,9 +189,7 @@ __device__ __forceinline__ void bond_one(const Dev<R>& d, uint32_t ia, uint32_t 
   R qy = qa.w * qb.y + qa.x * qb.z - qa.y * qb.w - qa.z * qb.x;
   R qz = qa.w * qb.z - qa.x * qb.y + qa.y * qb.x - qa.z * qb.w;
   if (qw < R(0)) { qw = -qw; qx = -qx; qy = -qy; qz = -qz; }
-  const R s = vx_sqrt(qx * qx + qy * qy + qz * qz);
-  const R k = s > R(0) ? R(2) * vx_atan2(s, qw) / s : R(0);
-  const V3<R> th = to_bond<AX>(mk(k * qx, k * qy, k * qz));
+  const V3<R> th = to_bond<AX>(rotvec_scale(qw, qx, qy, qz) * mk(qx, qy, qz));
 
   // Eq. 40: X2 = d_x - L_T with L_T = l (1 + alpha_mean dT)
   const R X2 = dv.x - l * c.alpha_mean * dT;
@@ -208,7 +225,7 @@ __device__ __forceinline__ void bond_one(const Dev<R>& d, uint32_t ia, uint32_t 
 }
 
 template <class R>
-__global__ void __launch_bounds__(256) k_bonds(Dev<R> d, uint32_t beg, uint32_t end) {
+__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 4 : 2) k_bonds(Dev<R> d, uint32_t beg, uint32_t end) {
   using R4 = typename VT<R>::R4;
   using R2 = typename VT<R>::R2;
   const uint32_t id = beg + blockIdx.x * blockDim.x + threadIdx.x;
