@@ -180,23 +180,18 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1212_2845_b200 import from_scene, nccl_unique_id
+    from paper_1212_2845_b200 import dist as vd
+    from paper_1212_2845_b200 import from_scene
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            print("use torchrun for --gpus > 1", file=sys.stderr)
-            return 2
+    world, rank, local = vd.env_ranks()
+    if world == 1 and args.gpus > 1:
+        print("use torchrun for --gpus > 1", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nid = None
     if world > 1:
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        nid = vd.bootstrap_nccl_id(dist, rank)
 
     sc = scene_for(args.config, args.precision)
     lat = from_scene(sc, precision=args.precision, device=local, rank=rank, nranks=world,
@@ -229,10 +224,7 @@ def run_ours(args):
     ms = ev0.elapsed_time(ev1)
     kt = lat.kernel_times()
     lat.set_instrumentation(False)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = vd.max_over_ranks([ms], dist if world > 1 else None, "cuda")[0]
     value = N * args.steps / (ms_max / 1e3)
 
     # ---- roofline of the dominant kernel (live CUDA-event durations)
@@ -287,10 +279,8 @@ def run_ours(args):
         barrier()
         tw = time.perf_counter() - tw
         ems = e0.elapsed_time(e1)
-        t = torch.tensor([ems, tw * 1e3], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ems = float(t[1].item())   # host wall clock bounds the device timeline
+        # host wall clock around the calls bounds the device timeline
+        ems = max(vd.max_over_ranks([ems, tw * 1e3], dist if world > 1 else None, "cuda"))
         bi = sum(a.nbytes for a in hin)
         bo = sum(a.nbytes for a in (hout.pos, hout.quat, hout.linmom, hout.angmom, hout.latch))
         e2e = {"value": N * K / (ems / 1e3), "unit": UNIT,

@@ -55,10 +55,19 @@ typedef struct {
   const uint8_t* cells;     /* nx*ny*nz, x-fastest; 0 = empty, k>=1 -> palette[k-1]    */
   int32_t precision;        /* 32 or 64: arithmetic type of the device path            */
   int32_t device;           /* CUDA device ordinal                                     */
-  int32_t rank, nranks;     /* slab decomposition along x (nranks >= 1)                */
+  int32_t rank, nranks;     /* slab decomposition along x (nranks >= 1, <= nx)         */
   const void* nccl_id;      /* 128-byte ncclUniqueId from vx_nccl_unique_id() on rank 0,
-                               broadcast by the caller; NULL when nranks == 1           */
+                               broadcast by the caller: one process per GPU, ghost planes
+                               by NCCL send/recv.  NULL with nranks > 1 (rank 0): the
+                               nranks slabs are emulated inside this one handle on one
+                               device (ghost planes by device copies) -- the same slab
+                               arithmetic, used to test bitwise slab invariance.        */
 } vx_lattice_desc;
+
+/* Planes [x_begin, x_end) of the x-slab of `rank` out of `nranks` over nx
+ * planes (balanced: floor(r nx / P) .. floor((r+1) nx / P)).  Host-only. */
+vx_status vx_slab_planes(int32_t nx, int32_t nranks, int32_t rank, int32_t* x_begin,
+                         int32_t* x_end);
 
 /* Material palette entry (App. B AddMat).
  * Invariants: E > 0, rho > 0, -1 < nu < 0.5, mu_s >= mu_d >= 0. */

@@ -84,6 +84,7 @@ SIGNATURES = {
     "vx_destroy": (None, [_P]),
     "vx_last_error": (ctypes.c_char_p, []),
     "vx_nccl_unique_id": (_I32, [_P]),
+    "vx_slab_planes": (_I32, [_I32, _I32, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "vx_abi_version": (_I32, []),
 }
 

@@ -1,6 +1,7 @@
 // voxsim.cu -- host side of the B200 voxel stepper: lattice builder (L1),
-// material tables (Eq. 1-12), step orchestration with CUDA graphs and the
-// NCCL x-slab halo (L3), and the C ABI of include/voxsim.h (L4).
+// material tables (Eq. 1-12), step orchestration with CUDA graphs, the x-slab
+// decomposition with NCCL (one slab per process) or in-process emulated
+// slabs (L3), and the C ABI of include/voxsim.h (L4).
 // Paper: Hiller & Lipson, arXiv:1212.2845.  Readings: DESIGN.md §3.
 #include "voxsim.h"
 #include "vx_kernels.cuh"
@@ -53,6 +54,7 @@ struct DevBuf {
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
   ~DevBuf() { release(); }
   void release() {
     if (p) cudaFree(p);
@@ -72,6 +74,25 @@ struct DevBuf {
 
 const double kPi = 3.14159265358979323846;
 
+inline size_t rsize(int prec) { return prec == 32 ? 4 : 8; }
+inline unsigned grid_of(long long n, int b = 256) { return (unsigned)((n + b - 1) / b); }
+
+// Balanced slab of rank r of P over nx planes: [x0, x1).
+inline void slab_planes(int nx, int P, int r, int* x0, int* x1) {
+  *x0 = (int)((long long)r * nx / P);
+  *x1 = (int)((long long)(r + 1) * nx / P);
+}
+
+// One x-slab of the lattice: owned planes [x0, x1) plus one ghost plane on
+// each side that exists, [xl0, xl1); its own SoA state and bond records.
+struct Slab {
+  int x0 = 0, x1 = 0, xl0 = 0, xl1 = 0;
+  uint32_t nloc = 0;
+  long long box_base = 0;              // xl0 * plane
+  DevBuf pos, quat, mom, ang, recA, recB, recC, fextd, cf, meta_d, ext_of_local;
+  std::vector<uint32_t> meta_static;   // static meta bits, local box order
+};
+
 }  // namespace
 
 struct vx_lattice {
@@ -80,16 +101,15 @@ struct vx_lattice {
   double l = 0, origin[3] = {0, 0, 0};
   int prec = 32;
   int device = 0, rank = 0, nranks = 1;
+  bool emulated = false;                  // nranks slabs in this process, no NCCL
   std::vector<uint8_t> cells;             // x-fastest
-  // slab of this rank
-  int x0 = 0, x1 = 0, xl0 = 0, xl1 = 0;
-  uint32_t nloc = 0, plane = 0;           // plane = ny * nz
-  long long box_base = 0;                 // xl0 * plane
+  uint32_t plane = 0;                     // ny * nz
   long long nbox = 0;                     // nx * plane (global)
+  std::vector<Slab> slabs;                // 1 (single / NCCL rank) or nranks (emulated)
+  int x0 = 0, x1 = 0;                     // planes this handle owns
   // counts (global)
   long long N = 0, nbonds = 0, nsurf = 0;
   std::vector<long long> box_of_ext;      // global box id of each external voxel
-  std::vector<uint32_t> meta_static;      // local box
   int max_cell = 0;
   // boundary (external order)
   std::vector<uint8_t> fixed;
@@ -104,10 +124,8 @@ struct vx_lattice {
   // device
   cudaStream_t stream = nullptr, comm_stream = nullptr;
   cudaEvent_t ev_k4 = nullptr, ev_halo = nullptr;
-  DevBuf pos, quat, mom, ang, recA, recB, recC, fextd, cf, mat, pair, clk, meta_d, box_of_ext_d;
-  DevBuf ext_of_local;                    // local box id -> external id (divergence reports)
-  DevBuf pair_w2, mat_w2;
-  // self collision
+  DevBuf mat, pair, clk, box_of_ext_d, pair_w2, mat_w2;
+  // self collision (single slab only)
   std::vector<int> surf_local;
   DevBuf surf_d, cellh, bcount, bstart, bitems, rowptr, col;
   int H = 0;
@@ -123,13 +141,16 @@ struct vx_lattice {
   // nccl
   ncclComm_t comm = nullptr;
   long long steps_done = 0;
-  long long rebuild_host = 0;
 
+  bool nccl() const { return nranks > 1 && !emulated; }
   bool collide() const { return env_set && env.self_collision && nsurf > 0; }
+  int bond_launches() const {
+    if (emulated) return (int)slabs.size();
+    return nranks > 1 ? 3 : 1;
+  }
   int launches_per_step() const {
-    int k = 3;  // clock, bonds, integrate
+    int k = 1 + bond_launches() + (int)slabs.size();  // clock, bonds, integrate
     if (collide()) k += 2;
-    if (nranks > 1) k += 1;  // bonds split in interior + boundary launches
     return k;
   }
   void clear_graphs() {
@@ -140,8 +161,6 @@ struct vx_lattice {
 
 namespace {
 
-inline size_t rsize(int prec) { return prec == 32 ? 4 : 8; }
-
 // ---------------------------------------------------------------- L1 builder
 vx_status build_topology(vx_lattice* h) {
   const int nx = h->nx, ny = h->ny, nz = h->nz;
@@ -151,7 +170,6 @@ vx_status build_topology(vx_lattice* h) {
   };
   // external ids: filled cells in x-fastest order (vx_lattice_desc.cells)
   h->box_of_ext.clear();
-  h->N = 0;
   h->max_cell = 0;
   for (int k = 0; k < nz; ++k)
     for (int j = 0; j < ny; ++j)
@@ -163,7 +181,7 @@ vx_status build_topology(vx_lattice* h) {
       }
   h->N = (long long)h->box_of_ext.size();
   // local box meta: material, filled, neighbour mask, surface
-  h->meta_static.assign(h->nloc, 0u);
+  for (auto& s : h->slabs) s.meta_static.assign(s.nloc, 0u);
   h->nbonds = 0;
   h->nsurf = 0;
   h->surf_local.clear();
@@ -185,35 +203,37 @@ vx_status build_topology(vx_lattice* h) {
           m |= M_SURF;
           ++h->nsurf;
         }
-        if (i >= h->xl0 && i < h->xl1) {
-          const uint32_t li = (uint32_t)(((long long)(i - h->xl0) * ny + j) * nz + k);
-          h->meta_static[li] = m;
-          if ((m & M_SURF) && i >= h->x0 && i < h->x1) h->surf_local.push_back((int)li);
+        for (auto& s : h->slabs) {
+          if (i < s.xl0 || i >= s.xl1) continue;
+          const uint32_t li = (uint32_t)(((long long)(i - s.xl0) * ny + j) * nz + k);
+          s.meta_static[li] = m;
+          if ((m & M_SURF) && h->slabs.size() == 1 && i >= s.x0 && i < s.x1)
+            h->surf_local.push_back((int)li);
         }
       }
   return VX_OK;
 }
 
-template <class R> Dev<R> make_dev(vx_lattice* h) {
+template <class R> Dev<R> make_dev(const vx_lattice* h, const Slab& s) {
   Dev<R> d;
-  d.pos = h->pos.as<typename VT<R>::R4>();
-  d.quat = h->quat.as<typename VT<R>::R4>();
-  d.mom = h->mom.as<typename VT<R>::R4>();
-  d.ang = h->ang.as<typename VT<R>::R2>();
-  d.recA = h->recA.as<typename VT<R>::R4>();
-  d.recB = h->recB.as<typename VT<R>::R4>();
-  d.recC = h->recC.as<R>();
-  d.fext = h->any_ext ? h->fextd.as<typename VT<R>::R4>() : nullptr;
-  d.cf = h->cf.as<typename VT<R>::R4>();
+  d.pos = s.pos.as<typename VT<R>::R4>();
+  d.quat = s.quat.as<typename VT<R>::R4>();
+  d.mom = s.mom.as<typename VT<R>::R4>();
+  d.ang = s.ang.as<typename VT<R>::R2>();
+  d.recA = s.recA.as<typename VT<R>::R4>();
+  d.recB = s.recB.as<typename VT<R>::R4>();
+  d.recC = s.recC.as<R>();
+  d.fext = h->any_ext ? s.fextd.as<typename VT<R>::R4>() : nullptr;
+  d.cf = s.cf.as<typename VT<R>::R4>();
   d.mat = h->mat.as<MatC<R>>();
   d.pair = h->pair.as<PairC<R>>();
   d.clk = h->clk.as<Clock>();
   d.nmat = (int)h->mats.size();
-  d.nloc = h->nloc;
+  d.nloc = s.nloc;
   d.sx = h->plane;
   d.ny = (uint32_t)h->ny;
   d.nz = (uint32_t)h->nz;
-  d.xl0 = h->xl0;
+  d.xl0 = s.xl0;
   d.l = (R)h->l;
   d.half_l = (R)(0.5 * h->l);
   d.dt = (R)h->dt;
@@ -224,42 +244,36 @@ template <class R> Dev<R> make_dev(vx_lattice* h) {
   return d;
 }
 
-inline unsigned grid_of(long long n, int b = 256) { return (unsigned)((n + b - 1) / b); }
-
 vx_status upload_meta(vx_lattice* h) {
   // static bits + boundary bits -> device, merged with the latch bits
-  std::vector<uint32_t> m(h->meta_static);
-  for (long long e = 0; e < h->N; ++e) {
-    const long long li = h->box_of_ext[e] - h->box_base;
-    if (li < 0 || li >= (long long)h->nloc) continue;
-    m[li] &= ~(M_FIXED | M_EXT);
-    if (!h->fixed.empty() && h->fixed[e]) m[li] |= M_FIXED;
-    if (h->any_ext && (h->fext[3 * e] != 0 || h->fext[3 * e + 1] != 0 || h->fext[3 * e + 2] != 0))
-      m[li] |= M_EXT;
-  }
-  VX_CUDA(cudaMemcpyAsync(h->meta_d.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  if (h->prec == 32)
-    k_merge_meta<float><<<grid_of(h->nloc), 256, 0, h->stream>>>(make_dev<float>(h), h->meta_d.as<uint32_t>(), h->nloc);
-  else
-    k_merge_meta<double><<<grid_of(h->nloc), 256, 0, h->stream>>>(make_dev<double>(h), h->meta_d.as<uint32_t>(), h->nloc);
-  VX_CUDA(cudaGetLastError());
-  // external forces (local box order)
-  if (h->any_ext) {
-    const size_t r4 = 4 * rsize(h->prec);
-    VX_TRY(h->fextd.alloc((size_t)h->nloc * r4));
-    std::vector<double> f4((size_t)h->nloc * 4, 0.0);
+  for (auto& s : h->slabs) {
+    std::vector<uint32_t> m(s.meta_static);
+    std::vector<double> f4;
+    if (h->any_ext) f4.assign((size_t)s.nloc * 4, 0.0);
     for (long long e = 0; e < h->N; ++e) {
-      const long long li = h->box_of_ext[e] - h->box_base;
-      if (li < 0 || li >= (long long)h->nloc) continue;
-      for (int c = 0; c < 3; ++c) f4[4 * li + c] = h->fext[3 * e + c];
+      const long long li = h->box_of_ext[e] - s.box_base;
+      if (li < 0 || li >= (long long)s.nloc) continue;
+      m[li] &= ~(M_FIXED | M_EXT);
+      if (!h->fixed.empty() && h->fixed[e]) m[li] |= M_FIXED;
+      if (h->any_ext && (h->fext[3 * e] != 0 || h->fext[3 * e + 1] != 0 || h->fext[3 * e + 2] != 0)) {
+        m[li] |= M_EXT;
+        for (int c = 0; c < 3; ++c) f4[4 * li + c] = h->fext[3 * e + c];
+      }
     }
-    if (h->prec == 32) {
-      std::vector<float> f(f4.begin(), f4.end());
-      VX_CUDA(cudaMemcpyAsync(h->fextd.p, f.data(), f.size() * 4, cudaMemcpyHostToDevice, h->stream));
-      VX_CUDA(cudaStreamSynchronize(h->stream));
-    } else {
-      VX_CUDA(cudaMemcpyAsync(h->fextd.p, f4.data(), f4.size() * 8, cudaMemcpyHostToDevice, h->stream));
-      VX_CUDA(cudaStreamSynchronize(h->stream));
+    VX_CUDA(cudaMemcpy(s.meta_d.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice));
+    if (h->prec == 32)
+      k_merge_meta<float><<<grid_of(s.nloc), 256, 0, h->stream>>>(make_dev<float>(h, s), s.meta_d.as<uint32_t>(), s.nloc);
+    else
+      k_merge_meta<double><<<grid_of(s.nloc), 256, 0, h->stream>>>(make_dev<double>(h, s), s.meta_d.as<uint32_t>(), s.nloc);
+    VX_CUDA(cudaGetLastError());
+    if (h->any_ext) {
+      VX_TRY(s.fextd.alloc((size_t)s.nloc * 4 * rsize(h->prec)));
+      if (h->prec == 32) {
+        std::vector<float> f(f4.begin(), f4.end());
+        VX_CUDA(cudaMemcpy(s.fextd.p, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+      } else {
+        VX_CUDA(cudaMemcpy(s.fextd.p, f4.data(), f4.size() * 8, cudaMemcpyHostToDevice));
+      }
     }
   }
   VX_CUDA(cudaStreamSynchronize(h->stream));
@@ -331,9 +345,8 @@ template <class R> vx_status upload_tables(vx_lattice* h) {
     }
   VX_TRY(h->mat.alloc(mc.size() * sizeof(MatC<R>)));
   VX_TRY(h->pair.alloc(pc.size() * sizeof(PairC<R>)));
-  VX_CUDA(cudaMemcpyAsync(h->mat.p, mc.data(), mc.size() * sizeof(MatC<R>), cudaMemcpyHostToDevice, h->stream));
-  VX_CUDA(cudaMemcpyAsync(h->pair.p, pc.data(), pc.size() * sizeof(PairC<R>), cudaMemcpyHostToDevice, h->stream));
-  VX_CUDA(cudaStreamSynchronize(h->stream));
+  VX_CUDA(cudaMemcpy(h->mat.p, mc.data(), mc.size() * sizeof(MatC<R>), cudaMemcpyHostToDevice));
+  VX_CUDA(cudaMemcpy(h->pair.p, pc.data(), pc.size() * sizeof(PairC<R>), cudaMemcpyHostToDevice));
   return VX_OK;
 }
 
@@ -353,13 +366,18 @@ template <class R> vx_status compute_dt(vx_lattice* h) {
   }
   VX_TRY(h->pair_w2.alloc(pw.size() * 8));
   VX_TRY(h->mat_w2.alloc(mw.size() * 8));
-  VX_CUDA(cudaMemcpyAsync(h->pair_w2.p, pw.data(), pw.size() * 8, cudaMemcpyHostToDevice, h->stream));
-  VX_CUDA(cudaMemcpyAsync(h->mat_w2.p, mw.data(), mw.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  VX_CUDA(cudaMemcpy(h->pair_w2.p, pw.data(), pw.size() * 8, cudaMemcpyHostToDevice));
+  VX_CUDA(cudaMemcpy(h->mat_w2.p, mw.data(), mw.size() * 8, cudaMemcpyHostToDevice));
   Clock* c = h->clk.as<Clock>();
   VX_CUDA(cudaMemsetAsync(&c->w2_bond_bits, 0, 16, h->stream));
-  k_dt<R><<<grid_of(h->nloc), 256, 0, h->stream>>>(h->pos.as<typename VT<R>::R4>(), 0u, h->nloc,
-                                                   h->plane, (uint32_t)h->nz, h->pair_w2.as<double>(),
-                                                   h->mat_w2.as<double>(), n, c);
+  for (auto& s : h->slabs) {
+    // planes [xl0, x1): the right ghost plane's +x bonds belong to the next slab
+    // (its +x neighbour is outside this slab's box)
+    const uint32_t end = (uint32_t)(s.x1 - s.xl0) * h->plane;
+    k_dt<R><<<grid_of(end), 256, 0, h->stream>>>(s.pos.as<typename VT<R>::R4>(), 0u, end,
+                                                 h->plane, (uint32_t)h->nz, h->pair_w2.as<double>(),
+                                                 h->mat_w2.as<double>(), n, c);
+  }
   VX_CUDA(cudaGetLastError());
   unsigned long long bits[2];
   VX_CUDA(cudaMemcpyAsync(bits, &c->w2_bond_bits, 16, cudaMemcpyDeviceToHost, h->stream));
@@ -367,15 +385,14 @@ template <class R> vx_status compute_dt(vx_lattice* h) {
   double wb, wv;
   std::memcpy(&wb, &bits[0], 8);
   std::memcpy(&wv, &bits[1], 8);
-  if (h->nranks > 1) {
-    double* tmp = nullptr;
-    VX_CUDA(cudaMalloc(&tmp, 16));
+  if (h->nccl()) {
+    DevBuf t;
+    VX_TRY(t.alloc(16));
     double hv[2] = {wb, wv};
-    VX_CUDA(cudaMemcpy(tmp, hv, 16, cudaMemcpyHostToDevice));
-    VX_NCCL(ncclAllReduce(tmp, tmp, 2, ncclDouble, ncclMax, h->comm, h->stream));
-    VX_CUDA(cudaMemcpyAsync(hv, tmp, 16, cudaMemcpyDeviceToHost, h->stream));
+    VX_CUDA(cudaMemcpy(t.p, hv, 16, cudaMemcpyHostToDevice));
+    VX_NCCL(ncclAllReduce(t.p, t.p, 2, ncclDouble, ncclMax, h->comm, h->stream));
+    VX_CUDA(cudaMemcpyAsync(hv, t.p, 16, cudaMemcpyDeviceToHost, h->stream));
     VX_CUDA(cudaStreamSynchronize(h->stream));
-    cudaFree(tmp);
     wb = hv[0];
     wv = hv[1];
   }
@@ -390,6 +407,7 @@ void update_dt(vx_lattice* h) {
 }
 
 vx_status setup_collision(vx_lattice* h) {
+  Slab& sl = h->slabs[0];
   const int S = (int)h->surf_local.size();
   VX_TRY(h->surf_d.alloc((size_t)std::max(S, 1) * 4));
   if (S) VX_CUDA(cudaMemcpy(h->surf_d.p, h->surf_local.data(), (size_t)S * 4, cudaMemcpyHostToDevice));
@@ -403,9 +421,9 @@ vx_status setup_collision(vx_lattice* h) {
   VX_TRY(h->bitems.alloc((size_t)std::max(S, 1) * 4));
   VX_TRY(h->rowptr.alloc((size_t)(S + 1) * 4));
   VX_TRY(h->col.alloc((size_t)h->cap * 4));
-  VX_TRY(h->cf.alloc((size_t)h->nloc * 4 * rsize(h->prec)));
+  VX_TRY(sl.cf.alloc((size_t)sl.nloc * 4 * rsize(h->prec)));
   VX_CUDA(cudaMemset(h->rowptr.p, 0, (size_t)(S + 1) * 4));
-  VX_CUDA(cudaMemset(h->cf.p, 0, h->cf.bytes));
+  VX_CUDA(cudaMemset(sl.cf.p, 0, sl.cf.bytes));
   // cutoff = 2 r_max + horizon, r_max = (l/2)(1 + max|alpha| |T_amp|)
   double amax = 0;
   for (auto& m : h->mats) amax = std::max(amax, std::fabs(m.cte));
@@ -429,47 +447,87 @@ vx_status prepare(vx_lattice* h) {
 }
 
 // ---------------------------------------------------------------- one step
-template <class R> void launch_bonds(vx_lattice* h, const Dev<R>& d, int p0, int p1) {
+template <class R>
+void launch_bonds(vx_lattice* h, const Slab& s, const Dev<R>& d, int p0, int p1) {
   if (p1 <= p0) return;
-  const uint32_t beg = (uint32_t)(p0 - h->xl0) * h->plane, end = (uint32_t)(p1 - h->xl0) * h->plane;
+  const uint32_t beg = (uint32_t)(p0 - s.xl0) * h->plane, end = (uint32_t)(p1 - s.xl0) * h->plane;
   k_bonds<R><<<grid_of(end - beg), 256, 0, h->stream>>>(d, beg, end);
 }
 
-template <class R> vx_status halo_exchange(vx_lattice* h) {
-  // ghost planes <- neighbours' boundary planes (state S_n), on comm_stream
-  const size_t pl = h->plane;
+template <class R> void launch_integrate(vx_lattice* h, const Slab& s, const Dev<R>& d, bool col) {
+  const uint32_t beg = (uint32_t)(s.x0 - s.xl0) * h->plane, end = (uint32_t)(s.x1 - s.xl0) * h->plane;
+  if (col)
+    k_integrate<R, true><<<grid_of(end - beg), 256, 0, h->stream>>>(d, beg, end, s.ext_of_local.as<uint32_t>());
+  else
+    k_integrate<R, false><<<grid_of(end - beg), 256, 0, h->stream>>>(d, beg, end, s.ext_of_local.as<uint32_t>());
+}
+
+// The four SoA state arrays of a slab, with element sizes.
+struct Arr {
+  char* base;
+  size_t esz;
+};
+void state_arrays(const vx_lattice* h, const Slab& s, Arr out[4]) {
   const size_t r = rsize(h->prec);
-  struct Arr { char* base; size_t esz; } arrs[4] = {
-      {h->pos.as<char>(), 4 * r}, {h->quat.as<char>(), 4 * r}, {h->mom.as<char>(), 4 * r},
-      {h->ang.as<char>(), 2 * r}};
+  out[0] = {s.pos.as<char>(), 4 * r};
+  out[1] = {s.quat.as<char>(), 4 * r};
+  out[2] = {s.mom.as<char>(), 4 * r};
+  out[3] = {s.ang.as<char>(), 2 * r};
+}
+inline char* plane_ptr(const Arr& a, const Slab& s, int x, size_t plane) {
+  return a.base + (size_t)(x - s.xl0) * plane * a.esz;
+}
+
+// NCCL ghost exchange of state S_n (one slab per rank), on comm_stream
+vx_status halo_nccl(vx_lattice* h) {
+  const Slab& s = h->slabs[0];
+  Arr arrs[4];
+  state_arrays(h, s, arrs);
   VX_NCCL(ncclGroupStart());
   for (auto& a : arrs) {
-    const size_t bytes = pl * a.esz;
-    if (h->x0 > 0) {   // left neighbour: send my first owned plane, receive ghost left
-      char* mine = a.base + (size_t)(h->x0 - h->xl0) * pl * a.esz;
-      char* ghost = a.base;
-      VX_NCCL(ncclSend(mine, bytes, ncclInt8, h->rank - 1, h->comm, h->comm_stream));
-      VX_NCCL(ncclRecv(ghost, bytes, ncclInt8, h->rank - 1, h->comm, h->comm_stream));
+    const size_t bytes = h->plane * a.esz;
+    if (s.x0 > 0) {   // left neighbour: send my first owned plane, receive my left ghost
+      VX_NCCL(ncclSend(plane_ptr(a, s, s.x0, h->plane), bytes, ncclInt8, h->rank - 1, h->comm, h->comm_stream));
+      VX_NCCL(ncclRecv(plane_ptr(a, s, s.x0 - 1, h->plane), bytes, ncclInt8, h->rank - 1, h->comm, h->comm_stream));
     }
-    if (h->x1 < h->nx) {   // right neighbour
-      char* mine = a.base + (size_t)(h->x1 - 1 - h->xl0) * pl * a.esz;
-      char* ghost = a.base + (size_t)(h->x1 - h->xl0) * pl * a.esz;
-      VX_NCCL(ncclSend(mine, bytes, ncclInt8, h->rank + 1, h->comm, h->comm_stream));
-      VX_NCCL(ncclRecv(ghost, bytes, ncclInt8, h->rank + 1, h->comm, h->comm_stream));
+    if (s.x1 < h->nx) {   // right neighbour
+      VX_NCCL(ncclSend(plane_ptr(a, s, s.x1 - 1, h->plane), bytes, ncclInt8, h->rank + 1, h->comm, h->comm_stream));
+      VX_NCCL(ncclRecv(plane_ptr(a, s, s.x1, h->plane), bytes, ncclInt8, h->rank + 1, h->comm, h->comm_stream));
     }
   }
   VX_NCCL(ncclGroupEnd());
   return VX_OK;
 }
 
+// Emulated slabs: ghost planes <- neighbouring slabs' owned planes (device copies)
+vx_status halo_local(vx_lattice* h) {
+  for (size_t q = 0; q < h->slabs.size(); ++q) {
+    const Slab& s = h->slabs[q];
+    Arr mine[4];
+    state_arrays(h, s, mine);
+    for (int side = 0; side < 2; ++side) {
+      const int nb = side == 0 ? (int)q - 1 : (int)q + 1;
+      if (nb < 0 || nb >= (int)h->slabs.size()) continue;
+      const Slab& o = h->slabs[nb];
+      Arr theirs[4];
+      state_arrays(h, o, theirs);
+      const int x = side == 0 ? s.x0 - 1 : s.x1;   // ghost plane = neighbour's owned plane
+      for (int a = 0; a < 4; ++a)
+        VX_CUDA(cudaMemcpyAsync(plane_ptr(mine[a], s, x, h->plane), plane_ptr(theirs[a], o, x, h->plane),
+                                h->plane * mine[a].esz, cudaMemcpyDeviceToDevice, h->stream));
+    }
+  }
+  return VX_OK;
+}
+
 template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
-  const Dev<R> d = make_dev<R>(h);
   const bool col = h->collide();
   if (ev) VX_CUDA(cudaEventRecord(ev[0], h->stream));
   ClockArgs ca{h->clk.as<Clock>(), h->dt, h->env.T_amp, h->env.T_freq, h->env.T_phase,
                0.5 * h->env.horizon_voxels * h->l, col ? 1 : 0, h->prec};
   k_clock<<<1, 32, 0, h->stream>>>(ca);
   if (col) {
+    const Dev<R> d = make_dev<R>(h, h->slabs[0]);
     BroadArgs b{h->surf_d.as<int>(), (int)h->surf_local.size(), h->cellh.as<int4>(),
                 h->bcount.as<int>(), h->bstart.as<int>(), h->bitems.as<int>(),
                 h->rowptr.as<int>(), h->col.as<int>(), h->cap, h->H, h->clk.as<Clock>()};
@@ -481,26 +539,25 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
       k_contact<R><<<grid_of(S), 256, 0, h->stream>>>(d, h->surf_d.as<int>(), S, h->rowptr.as<int>(),
                                                       h->col.as<int>(), (R)h->env.zeta_col);
   }
+  if (h->emulated) VX_TRY(halo_local(h));
   if (ev) VX_CUDA(cudaEventRecord(ev[1], h->stream));
-  if (h->nranks == 1) {
-    launch_bonds<R>(h, d, h->xl0, h->xl1);
-  } else {
-    // halo of S_n on the comm stream overlapped with the interior bonds
+  if (h->nccl()) {
+    // halo of S_n on the comm stream, overlapped with the interior bonds
+    const Slab& s = h->slabs[0];
+    const Dev<R> d = make_dev<R>(h, s);
     VX_CUDA(cudaEventRecord(h->ev_k4, h->stream));
     VX_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_k4, 0));
-    VX_TRY(halo_exchange<R>(h));
+    VX_TRY(halo_nccl(h));
     VX_CUDA(cudaEventRecord(h->ev_halo, h->comm_stream));
-    launch_bonds<R>(h, d, h->x0, h->x1 - 1);
+    launch_bonds<R>(h, s, d, s.x0, s.x1 - 1);
     VX_CUDA(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
-    if (h->xl0 < h->x0) launch_bonds<R>(h, d, h->xl0, h->x0);
-    launch_bonds<R>(h, d, h->x1 - 1, h->x1);
+    launch_bonds<R>(h, s, d, s.xl0, s.x0);
+    launch_bonds<R>(h, s, d, s.x1 - 1, s.x1);
+  } else {
+    for (const Slab& s : h->slabs) launch_bonds<R>(h, s, make_dev<R>(h, s), s.xl0, s.x1);
   }
   if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
-  const uint32_t beg = (uint32_t)(h->x0 - h->xl0) * h->plane, end = (uint32_t)(h->x1 - h->xl0) * h->plane;
-  if (col)
-    k_integrate<R, true><<<grid_of(end - beg), 256, 0, h->stream>>>(d, beg, end, h->ext_of_local.as<uint32_t>());
-  else
-    k_integrate<R, false><<<grid_of(end - beg), 256, 0, h->stream>>>(d, beg, end, h->ext_of_local.as<uint32_t>());
+  for (const Slab& s : h->slabs) launch_integrate<R>(h, s, make_dev<R>(h, s), col);
   if (ev) VX_CUDA(cudaEventRecord(ev[3], h->stream));
   VX_CUDA(cudaGetLastError());
   return VX_OK;
@@ -524,8 +581,8 @@ template <class R> vx_status run_steps(vx_lattice* h, long long n) {
       VX_CUDA(cudaEventElapsedTime(&c, e[0], e[1]));
       VX_CUDA(cudaEventElapsedTime(&t, e[0], e[3]));
       h->t_ms[0] += a; h->t_ms[1] += b; h->t_ms[2] += c; h->t_ms[3] += t;
-      h->t_cnt[0] += h->nranks > 1 ? 3 : 1;
-      h->t_cnt[1] += 1;
+      h->t_cnt[0] += h->bond_launches();
+      h->t_cnt[1] += (long long)h->slabs.size();
       h->t_cnt[2] += h->collide() ? 3 : 1;
       h->t_cnt[3] += h->launches_per_step();
     }
@@ -572,7 +629,40 @@ vx_status set_device(const vx_lattice* h) {
   return VX_OK;
 }
 
-vx_status read_box(vx_lattice* h, double* boxbuf);
+vx_status set_force_rebuild(vx_lattice* h) {
+  Clock* c = h->clk.as<Clock>();
+  int one = 1;
+  VX_CUDA(cudaMemcpy(&c->force_rebuild, &one, 4, cudaMemcpyHostToDevice));
+  return VX_OK;
+}
+
+// Owned planes -> box-ordered fp64 SoA (14 components x nbox) on every rank.
+vx_status read_box(vx_lattice* h, double* boxbuf) {
+  for (const Slab& s : h->slabs) {
+    const uint32_t beg = (uint32_t)(s.x0 - s.xl0) * h->plane, end = (uint32_t)(s.x1 - s.xl0) * h->plane;
+    if (h->prec == 32)
+      k_pack_box<float><<<grid_of(end - beg), 256, 0, h->stream>>>(make_dev<float>(h, s), beg, end, s.box_base,
+                                                                   h->nbox, boxbuf, h->origin[0], h->origin[1], h->origin[2]);
+    else
+      k_pack_box<double><<<grid_of(end - beg), 256, 0, h->stream>>>(make_dev<double>(h, s), beg, end, s.box_base,
+                                                                    h->nbox, boxbuf, h->origin[0], h->origin[1], h->origin[2]);
+    VX_CUDA(cudaGetLastError());
+  }
+  if (h->nccl()) {
+    VX_NCCL(ncclGroupStart());
+    for (int r = 0; r < h->nranks; ++r) {
+      int x0, x1;
+      slab_planes(h->nx, h->nranks, r, &x0, &x1);
+      const size_t cnt = (size_t)(x1 - x0) * h->plane;
+      for (int c = 0; c < 14; ++c) {
+        double* p = boxbuf + (size_t)c * h->nbox + (size_t)x0 * h->plane;
+        VX_NCCL(ncclBroadcast(p, p, cnt, ncclDouble, r, h->comm, h->stream));
+      }
+    }
+    VX_NCCL(ncclGroupEnd());
+  }
+  return VX_OK;
+}
 
 }  // namespace
 
@@ -581,6 +671,13 @@ extern "C" {
 
 const char* vx_last_error(void) { return g_err.c_str(); }
 int32_t vx_abi_version(void) { return VOXSIM_ABI_VERSION; }
+
+vx_status vx_slab_planes(int32_t nx, int32_t nranks, int32_t rank, int32_t* x_begin, int32_t* x_end) {
+  if (nx < 1 || nranks < 1 || nranks > nx || rank < 0 || rank >= nranks || !x_begin || !x_end)
+    return fail(VX_ERR_INVALID_ARG, "bad slab arguments");
+  slab_planes(nx, nranks, rank, x_begin, x_end);
+  return VX_OK;
+}
 
 vx_status vx_nccl_unique_id(void* out128) {
   if (!out128) return fail(VX_ERR_INVALID_ARG, "out128 is NULL");
@@ -604,7 +701,9 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   if (desc->nranks < 1 || desc->rank < 0 || desc->rank >= desc->nranks)
     return fail(VX_ERR_INVALID_ARG, "bad rank / nranks");
   if (desc->nranks > desc->nx) return fail(VX_ERR_INVALID_ARG, "nranks > nx (empty slab)");
-  if (desc->nranks > 1 && !desc->nccl_id) return fail(VX_ERR_INVALID_ARG, "nccl_id is NULL");
+  const bool emulated = desc->nranks > 1 && !desc->nccl_id;
+  if (emulated && desc->rank != 0)
+    return fail(VX_ERR_INVALID_ARG, "emulated slabs (nccl_id NULL) need rank 0");
   const long long cells = (long long)desc->nx * desc->ny * desc->nz;
   if (cells >= (1LL << 32)) return fail(VX_ERR_INVALID_ARG, "workspace too large (>= 2^32 cells)");
   VX_TRY(check_device());
@@ -614,15 +713,22 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   for (int c = 0; c < 3; ++c) h->origin[c] = desc->origin[c];
   h->prec = desc->precision;
   h->device = desc->device; h->rank = desc->rank; h->nranks = desc->nranks;
+  h->emulated = emulated;
   h->cells.assign(desc->cells, desc->cells + cells);
-  h->x0 = (int)((long long)h->rank * h->nx / h->nranks);
-  h->x1 = (int)((long long)(h->rank + 1) * h->nx / h->nranks);
-  h->xl0 = std::max(h->x0 - 1, 0);
-  h->xl1 = std::min(h->x1 + 1, h->nx);
   h->plane = (uint32_t)((long long)h->ny * h->nz);
-  h->nloc = (uint32_t)((long long)(h->xl1 - h->xl0) * h->plane);
-  h->box_base = (long long)h->xl0 * h->plane;
   h->nbox = (long long)h->nx * h->plane;
+  const int nslab = emulated ? h->nranks : 1;
+  h->slabs.resize(nslab);
+  for (int q = 0; q < nslab; ++q) {
+    Slab& s = h->slabs[q];
+    slab_planes(h->nx, h->nranks, emulated ? q : h->rank, &s.x0, &s.x1);
+    s.xl0 = std::max(s.x0 - 1, 0);
+    s.xl1 = std::min(s.x1 + 1, h->nx);
+    s.nloc = (uint32_t)((long long)(s.xl1 - s.xl0) * h->plane);
+    s.box_base = (long long)s.xl0 * h->plane;
+  }
+  h->x0 = h->slabs.front().x0;
+  h->x1 = h->slabs.back().x1;
   auto bail = [&](vx_status s) { std::string m = g_err; vx_destroy(h); g_err = m; return s; };
   vx_status s = set_device(h);
   if (s != VX_OK) return bail(s);
@@ -631,37 +737,35 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
       cudaEventCreateWithFlags(&h->ev_k4, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(VX_ERR_CUDA, "stream/event creation failed"));
-  s = build_topology(h);
-  if (s != VX_OK) return bail(s);
-  const size_t r = rsize(h->prec), n = h->nloc;
-  if ((s = h->pos.alloc(n * 4 * r)) || (s = h->quat.alloc(n * 4 * r)) || (s = h->mom.alloc(n * 4 * r)) ||
-      (s = h->ang.alloc(n * 2 * r)) || (s = h->recA.alloc(3 * n * 4 * r)) ||
-      (s = h->recB.alloc(3 * n * 4 * r)) || (s = h->recC.alloc(3 * n * r)) ||
-      (s = h->clk.alloc(sizeof(Clock))) || (s = h->meta_d.alloc(n * 4)) ||
-      (s = h->box_of_ext_d.alloc((size_t)std::max<long long>(h->N, 1) * 8)) ||
-      (s = h->ext_of_local.alloc(n * 4)))
+  if ((s = build_topology(h)) != VX_OK) return bail(s);
+  const size_t r = rsize(h->prec);
+  if ((s = h->clk.alloc(sizeof(Clock))) ||
+      (s = h->box_of_ext_d.alloc((size_t)std::max<long long>(h->N, 1) * 8)))
     return bail(s);
-  {
-    std::vector<uint32_t> eol(n, 0xffffffffu);
-    for (long long e = 0; e < h->N; ++e) {
-      const long long li = h->box_of_ext[e] - h->box_base;
-      if (li >= 0 && li < (long long)n) eol[li] = (uint32_t)e;
-    }
-    if (cudaMemcpy(h->ext_of_local.p, eol.data(), n * 4, cudaMemcpyHostToDevice) != cudaSuccess)
-      return bail(fail(VX_ERR_CUDA, "upload failed"));
-  }
-  // initial state: at rest on the lattice sites, identity orientation
-  if (cudaMemset(h->pos.p, 0, h->pos.bytes) != cudaSuccess || cudaMemset(h->mom.p, 0, h->mom.bytes) != cudaSuccess ||
-      cudaMemset(h->ang.p, 0, h->ang.bytes) != cudaSuccess || cudaMemset(h->recA.p, 0, h->recA.bytes) != cudaSuccess ||
-      cudaMemset(h->recB.p, 0, h->recB.bytes) != cudaSuccess || cudaMemset(h->recC.p, 0, h->recC.bytes) != cudaSuccess)
-    return bail(fail(VX_ERR_CUDA, "memset failed"));
-  {
-    std::vector<char> q(h->quat.bytes, 0);
+  for (Slab& sl : h->slabs) {
+    const size_t n = sl.nloc;
+    if ((s = sl.pos.alloc(n * 4 * r)) || (s = sl.quat.alloc(n * 4 * r)) || (s = sl.mom.alloc(n * 4 * r)) ||
+        (s = sl.ang.alloc(n * 2 * r)) || (s = sl.recA.alloc(3 * n * 4 * r)) ||
+        (s = sl.recB.alloc(3 * n * 4 * r)) || (s = sl.recC.alloc(3 * n * r)) ||
+        (s = sl.meta_d.alloc(n * 4)) || (s = sl.ext_of_local.alloc(n * 4)))
+      return bail(s);
+    // initial state: at rest on the lattice sites, identity orientation (.w = 1)
+    if (cudaMemset(sl.pos.p, 0, sl.pos.bytes) != cudaSuccess || cudaMemset(sl.mom.p, 0, sl.mom.bytes) != cudaSuccess ||
+        cudaMemset(sl.ang.p, 0, sl.ang.bytes) != cudaSuccess || cudaMemset(sl.recA.p, 0, sl.recA.bytes) != cudaSuccess ||
+        cudaMemset(sl.recB.p, 0, sl.recB.bytes) != cudaSuccess || cudaMemset(sl.recC.p, 0, sl.recC.bytes) != cudaSuccess)
+      return bail(fail(VX_ERR_CUDA, "memset failed"));
+    std::vector<char> q(sl.quat.bytes, 0);
     for (size_t i = 0; i < n; ++i) {
       if (r == 4) { float one = 1.f; std::memcpy(&q[i * 16 + 12], &one, 4); }
       else { double one = 1.0; std::memcpy(&q[i * 32 + 24], &one, 8); }
     }
-    if (cudaMemcpy(h->quat.p, q.data(), q.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    std::vector<uint32_t> eol(n, 0xffffffffu);
+    for (long long e = 0; e < h->N; ++e) {
+      const long long li = h->box_of_ext[e] - sl.box_base;
+      if (li >= 0 && li < (long long)n) eol[li] = (uint32_t)e;
+    }
+    if (cudaMemcpy(sl.quat.p, q.data(), q.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(sl.ext_of_local.p, eol.data(), n * 4, cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(VX_ERR_CUDA, "upload failed"));
   }
   Clock c0{};
@@ -673,7 +777,7 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   h->fixed.assign((size_t)h->N, 0);
   h->fext.assign((size_t)h->N * 3, 0.0);
   if ((s = upload_meta(h)) != VX_OK) return bail(s);
-  if (h->nranks > 1) {
+  if (h->nccl()) {
     ncclUniqueId id;
     std::memcpy(&id, desc->nccl_id, sizeof id);
     ncclResult_t nr = ncclCommInitRank(&h->comm, h->nranks, id, h->rank);
@@ -715,9 +819,7 @@ vx_status vx_set_materials(vx_lattice* h, const vx_material* p, int32_t n) {
   else VX_TRY(compute_dt<double>(h));
   h->mats_set = true;
   h->tables_dirty = true;
-  Clock* c = h->clk.as<Clock>();
-  int one = 1;
-  VX_CUDA(cudaMemcpy(&c->force_rebuild, &one, 4, cudaMemcpyHostToDevice));
+  VX_TRY(set_force_rebuild(h));
   update_dt(h);
   return VX_OK;
 }
@@ -740,9 +842,7 @@ vx_status vx_set_environment(vx_lattice* h, const vx_env* e) {
   h->env_set = true;
   h->tables_dirty = true;
   update_dt(h);
-  Clock* c = h->clk.as<Clock>();
-  int one = 1;
-  VX_CUDA(cudaMemcpy(&c->force_rebuild, &one, 4, cudaMemcpyHostToDevice));
+  VX_TRY(set_force_rebuild(h));
   h->clear_graphs();
   return VX_OK;
 }
@@ -750,17 +850,18 @@ vx_status vx_set_environment(vx_lattice* h, const vx_env* e) {
 vx_status vx_set_boundary(vx_lattice* h, const uint8_t* fixed, const double* f_ext) {
   if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
   VX_TRY(set_device(h));
-  h->fixed.assign((size_t)h->N, 0);
-  h->fext.assign((size_t)h->N * 3, 0.0);
-  if (fixed) std::copy(fixed, fixed + h->N, h->fixed.begin());
-  h->any_ext = false;
-  if (f_ext) {
+  std::vector<double> fe((size_t)h->N * 3, 0.0);
+  bool any = false;
+  if (f_ext)
     for (long long i = 0; i < 3 * h->N; ++i) {
       if (!std::isfinite(f_ext[i])) return fail(VX_ERR_INVALID_ARG, "non-finite external force");
-      h->fext[i] = f_ext[i];
-      h->any_ext |= f_ext[i] != 0;
+      fe[i] = f_ext[i];
+      any |= f_ext[i] != 0;
     }
-  }
+  h->fixed.assign((size_t)h->N, 0);
+  if (fixed) std::copy(fixed, fixed + h->N, h->fixed.begin());
+  h->fext.swap(fe);
+  h->any_ext = any;
   return upload_meta(h);
 }
 
@@ -816,22 +917,21 @@ vx_status vx_set_state(vx_lattice* h, const double* pos, const double* quat, con
   if (ang) VX_CUDA(cudaMemcpyAsync(bd + off[3], ang, (size_t)N * 24, cudaMemcpyHostToDevice, h->stream));
   if (latch) VX_CUDA(cudaMemcpyAsync(bl, latch, (size_t)N, cudaMemcpyHostToDevice, h->stream));
   const long long* boe = h->box_of_ext_d.as<long long>();
-  if (h->prec == 32)
-    k_scatter_state<float><<<grid_of(N), 256, 0, h->stream>>>(
-        make_dev<float>(h), boe, N, h->box_base, pos ? bd + off[0] : nullptr, quat ? bd + off[1] : nullptr,
-        lin ? bd + off[2] : nullptr, ang ? bd + off[3] : nullptr, latch ? bl : nullptr, h->origin[0],
-        h->origin[1], h->origin[2]);
-  else
-    k_scatter_state<double><<<grid_of(N), 256, 0, h->stream>>>(
-        make_dev<double>(h), boe, N, h->box_base, pos ? bd + off[0] : nullptr, quat ? bd + off[1] : nullptr,
-        lin ? bd + off[2] : nullptr, ang ? bd + off[3] : nullptr, latch ? bl : nullptr, h->origin[0],
-        h->origin[1], h->origin[2]);
-  VX_CUDA(cudaGetLastError());
-  Clock* c = h->clk.as<Clock>();
-  int one = 1;
-  VX_CUDA(cudaMemcpyAsync(&c->force_rebuild, &one, 4, cudaMemcpyHostToDevice, h->stream));
+  for (const Slab& s : h->slabs) {   // owned and ghost planes alike
+    if (h->prec == 32)
+      k_scatter_state<float><<<grid_of(N), 256, 0, h->stream>>>(
+          make_dev<float>(h, s), boe, N, s.box_base, pos ? bd + off[0] : nullptr, quat ? bd + off[1] : nullptr,
+          lin ? bd + off[2] : nullptr, ang ? bd + off[3] : nullptr, latch ? bl : nullptr, h->origin[0],
+          h->origin[1], h->origin[2]);
+    else
+      k_scatter_state<double><<<grid_of(N), 256, 0, h->stream>>>(
+          make_dev<double>(h, s), boe, N, s.box_base, pos ? bd + off[0] : nullptr, quat ? bd + off[1] : nullptr,
+          lin ? bd + off[2] : nullptr, ang ? bd + off[3] : nullptr, latch ? bl : nullptr, h->origin[0],
+          h->origin[1], h->origin[2]);
+    VX_CUDA(cudaGetLastError());
+  }
   VX_CUDA(cudaStreamSynchronize(h->stream));
-  return VX_OK;
+  return set_force_rebuild(h);
 }
 
 namespace {
@@ -840,26 +940,34 @@ struct CkptHeader {
   int32_t prec, rank;
   int64_t nloc, N, steps_done;
 };
-const uint64_t kCkptMagic = 0x31504b43584f56ULL;  // "VOXCKP1"
+const uint64_t kCkptMagic = 0x32504b43584f56ULL;  // "VOXCKP2"
+int64_t ckpt_nloc(const vx_lattice* h) {
+  int64_t n = 0;
+  for (const Slab& s : h->slabs) n += s.nloc;
+  return n;
+}
 }  // namespace
 
 int64_t vx_checkpoint_bytes(const vx_lattice* h) {
   if (!h) return -1;
-  return (int64_t)(sizeof(CkptHeader) + h->pos.bytes + h->quat.bytes + h->mom.bytes +
-                   h->ang.bytes + sizeof(Clock));
+  int64_t b = sizeof(CkptHeader) + sizeof(Clock);
+  for (const Slab& s : h->slabs) b += (int64_t)(s.pos.bytes + s.quat.bytes + s.mom.bytes + s.ang.bytes);
+  return b;
 }
 
 vx_status vx_save_checkpoint(vx_lattice* h, void* buf, int64_t bytes) {
   if (!h || !buf || bytes < vx_checkpoint_bytes(h)) return fail(VX_ERR_INVALID_ARG, "bad checkpoint buffer");
   VX_TRY(set_device(h));
   char* p = static_cast<char*>(buf);
-  CkptHeader hd{kCkptMagic, h->prec, h->rank, (int64_t)h->nloc, h->N, h->steps_done};
+  CkptHeader hd{kCkptMagic, h->prec, h->rank, ckpt_nloc(h), h->N, h->steps_done};
   std::memcpy(p, &hd, sizeof hd);
   p += sizeof hd;
-  for (DevBuf* b : {&h->pos, &h->quat, &h->mom, &h->ang, &h->clk}) {
-    VX_CUDA(cudaMemcpy(p, b->p, b->bytes, cudaMemcpyDeviceToHost));
-    p += b->bytes;
-  }
+  for (Slab& s : h->slabs)
+    for (DevBuf* b : {&s.pos, &s.quat, &s.mom, &s.ang}) {
+      VX_CUDA(cudaMemcpy(p, b->p, b->bytes, cudaMemcpyDeviceToHost));
+      p += b->bytes;
+    }
+  VX_CUDA(cudaMemcpy(p, h->clk.p, sizeof(Clock), cudaMemcpyDeviceToHost));
   return VX_OK;
 }
 
@@ -869,14 +977,15 @@ vx_status vx_load_checkpoint(vx_lattice* h, const void* buf, int64_t bytes) {
   const char* p = static_cast<const char*>(buf);
   CkptHeader hd;
   std::memcpy(&hd, p, sizeof hd);
-  if (hd.magic != kCkptMagic || hd.prec != h->prec || hd.nloc != (int64_t)h->nloc || hd.N != h->N ||
+  if (hd.magic != kCkptMagic || hd.prec != h->prec || hd.nloc != ckpt_nloc(h) || hd.N != h->N ||
       hd.rank != h->rank)
     return fail(VX_ERR_INVALID_ARG, "checkpoint does not match this lattice (shape, precision or rank)");
   p += sizeof hd;
-  for (DevBuf* b : {&h->pos, &h->quat, &h->mom, &h->ang}) {
-    VX_CUDA(cudaMemcpy(b->p, p, b->bytes, cudaMemcpyHostToDevice));
-    p += b->bytes;
-  }
+  for (Slab& s : h->slabs)
+    for (DevBuf* b : {&s.pos, &s.quat, &s.mom, &s.ang}) {
+      VX_CUDA(cudaMemcpy(b->p, p, b->bytes, cudaMemcpyHostToDevice));
+      p += b->bytes;
+    }
   Clock c;
   std::memcpy(&c, p, sizeof c);
   c.force_rebuild = 1;   // the pair list is rebuilt from the restored state
@@ -912,15 +1021,14 @@ vx_status vx_step(vx_lattice* h, int64_t n) {
   VX_CUDA(cudaMemcpy(&c, h->clk.p, sizeof c, cudaMemcpyDeviceToHost));
   unsigned long long err = c.err;
   int fault = c.fault, overflow = c.overflow;
-  if (h->nranks > 1) {
-    unsigned long long* t = nullptr;
-    VX_CUDA(cudaMalloc(&t, 24));
+  if (h->nccl()) {   // every rank returns the same status
+    DevBuf t;
+    VX_TRY(t.alloc(24));
     unsigned long long hv[3] = {err, ~0ULL - (unsigned long long)fault, ~0ULL - (unsigned long long)overflow};
-    VX_CUDA(cudaMemcpy(t, hv, 24, cudaMemcpyHostToDevice));
-    VX_NCCL(ncclAllReduce(t, t, 3, ncclUint64, ncclMin, h->comm, h->stream));
-    VX_CUDA(cudaMemcpyAsync(hv, t, 24, cudaMemcpyDeviceToHost, h->stream));
+    VX_CUDA(cudaMemcpy(t.p, hv, 24, cudaMemcpyHostToDevice));
+    VX_NCCL(ncclAllReduce(t.p, t.p, 3, ncclUint64, ncclMin, h->comm, h->stream));
+    VX_CUDA(cudaMemcpyAsync(hv, t.p, 24, cudaMemcpyDeviceToHost, h->stream));
     VX_CUDA(cudaStreamSynchronize(h->stream));
-    cudaFree(t);
     err = hv[0];
     fault = (int)(~0ULL - hv[1]);
     overflow = (int)(~0ULL - hv[2]);
@@ -934,37 +1042,6 @@ vx_status vx_step(vx_lattice* h, int64_t n) {
   }
   return VX_OK;
 }
-
-}  // extern "C"
-
-namespace {
-// Owned planes -> box-ordered fp64 SoA on every rank (ncclBroadcast per rank).
-vx_status read_box(vx_lattice* h, double* boxbuf) {
-  const uint32_t beg = (uint32_t)(h->x0 - h->xl0) * h->plane, end = (uint32_t)(h->x1 - h->xl0) * h->plane;
-  if (h->prec == 32)
-    k_pack_box<float><<<grid_of(end - beg), 256, 0, h->stream>>>(make_dev<float>(h), beg, end, h->box_base,
-                                                                 h->nbox, boxbuf, h->origin[0], h->origin[1], h->origin[2]);
-  else
-    k_pack_box<double><<<grid_of(end - beg), 256, 0, h->stream>>>(make_dev<double>(h), beg, end, h->box_base,
-                                                                  h->nbox, boxbuf, h->origin[0], h->origin[1], h->origin[2]);
-  VX_CUDA(cudaGetLastError());
-  if (h->nranks > 1) {
-    VX_NCCL(ncclGroupStart());
-    for (int r = 0; r < h->nranks; ++r) {
-      const long long x0 = (long long)r * h->nx / h->nranks, x1 = (long long)(r + 1) * h->nx / h->nranks;
-      const size_t cnt = (size_t)((x1 - x0) * h->plane);
-      for (int c = 0; c < 14; ++c) {
-        double* p = boxbuf + (size_t)c * h->nbox + (size_t)x0 * h->plane;
-        VX_NCCL(ncclBroadcast(p, p, cnt, ncclDouble, r, h->comm, h->stream));
-      }
-    }
-    VX_NCCL(ncclGroupEnd());
-  }
-  return VX_OK;
-}
-}  // namespace
-
-extern "C" {
 
 vx_status vx_read_state(vx_lattice* h, double* pos, double* quat, double* lin, double* ang,
                         uint8_t* latch) {
@@ -995,36 +1072,63 @@ vx_status vx_read_voxels(vx_lattice* h, const int64_t* ids, int64_t n, double* p
   if (!h || (n > 0 && !ids) || n < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
   if (n == 0) return VX_OK;
   VX_TRY(set_device(h));
-  std::vector<long long> lid((size_t)n), gid((size_t)n);
+  // group the requests by slab
+  std::vector<std::vector<int64_t>> which(h->slabs.size());
   for (int64_t i = 0; i < n; ++i) {
     if (ids[i] < 0 || ids[i] >= h->N) return fail(VX_ERR_OUT_OF_RANGE, "voxel id out of range");
-    const long long g = h->box_of_ext[ids[i]];
-    const long long x = g / h->plane;
-    if (x < h->x0 || x >= h->x1) return fail(VX_ERR_OUT_OF_RANGE, "voxel not owned by this rank");
-    gid[i] = g;
-    lid[i] = g - h->box_base;
+    const long long x = h->box_of_ext[ids[i]] / h->plane;
+    int q = -1;
+    for (size_t k = 0; k < h->slabs.size(); ++k)
+      if (x >= h->slabs[k].x0 && x < h->slabs[k].x1) q = (int)k;
+    if (q < 0) return fail(VX_ERR_OUT_OF_RANGE, "voxel not owned by this rank");
+    which[q].push_back(i);
   }
-  DevBuf ib, ob;
-  VX_TRY(ib.alloc((size_t)n * 16));
-  VX_TRY(ob.alloc((size_t)n * 13 * 8 + (size_t)n));
-  long long* dl = ib.as<long long>();
-  VX_CUDA(cudaMemcpyAsync(dl, lid.data(), (size_t)n * 8, cudaMemcpyHostToDevice, h->stream));
-  VX_CUDA(cudaMemcpyAsync(dl + n, gid.data(), (size_t)n * 8, cudaMemcpyHostToDevice, h->stream));
-  double* o = ob.as<double>();
-  uint8_t* ol = reinterpret_cast<uint8_t*>(o + (size_t)n * 13);
-  if (h->prec == 32)
-    k_read_ids<float><<<grid_of(n), 256, 0, h->stream>>>(make_dev<float>(h), dl, dl + n, n, o, o + n * 3, o + n * 7,
-                                                         o + n * 10, ol, h->origin[0], h->origin[1], h->origin[2]);
-  else
-    k_read_ids<double><<<grid_of(n), 256, 0, h->stream>>>(make_dev<double>(h), dl, dl + n, n, o, o + n * 3, o + n * 7,
-                                                          o + n * 10, ol, h->origin[0], h->origin[1], h->origin[2]);
-  VX_CUDA(cudaGetLastError());
-  if (pos) VX_CUDA(cudaMemcpyAsync(pos, o, (size_t)n * 24, cudaMemcpyDeviceToHost, h->stream));
-  if (quat) VX_CUDA(cudaMemcpyAsync(quat, o + n * 3, (size_t)n * 32, cudaMemcpyDeviceToHost, h->stream));
-  if (lin) VX_CUDA(cudaMemcpyAsync(lin, o + n * 7, (size_t)n * 24, cudaMemcpyDeviceToHost, h->stream));
-  if (ang) VX_CUDA(cudaMemcpyAsync(ang, o + n * 10, (size_t)n * 24, cudaMemcpyDeviceToHost, h->stream));
-  if (latch) VX_CUDA(cudaMemcpyAsync(latch, ol, (size_t)n, cudaMemcpyDeviceToHost, h->stream));
-  VX_CUDA(cudaStreamSynchronize(h->stream));
+  std::vector<double> hp((size_t)n * 13);
+  std::vector<uint8_t> hl((size_t)n);
+  for (size_t q = 0; q < h->slabs.size(); ++q) {
+    const std::vector<int64_t>& w = which[q];
+    const long long m = (long long)w.size();
+    if (!m) continue;
+    const Slab& s = h->slabs[q];
+    std::vector<long long> lid(m), gid(m);
+    for (long long i = 0; i < m; ++i) {
+      gid[i] = h->box_of_ext[ids[w[i]]];
+      lid[i] = gid[i] - s.box_base;
+    }
+    DevBuf ib, ob;
+    VX_TRY(ib.alloc((size_t)m * 16));
+    VX_TRY(ob.alloc((size_t)m * 13 * 8 + (size_t)m));
+    long long* dl = ib.as<long long>();
+    VX_CUDA(cudaMemcpy(dl, lid.data(), (size_t)m * 8, cudaMemcpyHostToDevice));
+    VX_CUDA(cudaMemcpy(dl + m, gid.data(), (size_t)m * 8, cudaMemcpyHostToDevice));
+    double* o = ob.as<double>();
+    uint8_t* ol = reinterpret_cast<uint8_t*>(o + (size_t)m * 13);
+    if (h->prec == 32)
+      k_read_ids<float><<<grid_of(m), 256, 0, h->stream>>>(make_dev<float>(h, s), dl, dl + m, m, o, o + m * 3, o + m * 7,
+                                                           o + m * 10, ol, h->origin[0], h->origin[1], h->origin[2]);
+    else
+      k_read_ids<double><<<grid_of(m), 256, 0, h->stream>>>(make_dev<double>(h, s), dl, dl + m, m, o, o + m * 3, o + m * 7,
+                                                            o + m * 10, ol, h->origin[0], h->origin[1], h->origin[2]);
+    VX_CUDA(cudaGetLastError());
+    std::vector<double> tmp((size_t)m * 13);
+    std::vector<uint8_t> tl((size_t)m);
+    VX_CUDA(cudaMemcpyAsync(tmp.data(), o, (size_t)m * 13 * 8, cudaMemcpyDeviceToHost, h->stream));
+    VX_CUDA(cudaMemcpyAsync(tl.data(), ol, (size_t)m, cudaMemcpyDeviceToHost, h->stream));
+    VX_CUDA(cudaStreamSynchronize(h->stream));
+    for (long long i = 0; i < m; ++i) {
+      const int64_t t = w[i];
+      for (int c = 0; c < 3; ++c) hp[(size_t)t * 3 + c] = tmp[(size_t)i * 3 + c];
+      for (int c = 0; c < 4; ++c) hp[(size_t)n * 3 + (size_t)t * 4 + c] = tmp[(size_t)m * 3 + (size_t)i * 4 + c];
+      for (int c = 0; c < 3; ++c) hp[(size_t)n * 7 + (size_t)t * 3 + c] = tmp[(size_t)m * 7 + (size_t)i * 3 + c];
+      for (int c = 0; c < 3; ++c) hp[(size_t)n * 10 + (size_t)t * 3 + c] = tmp[(size_t)m * 10 + (size_t)i * 3 + c];
+      hl[t] = tl[i];
+    }
+  }
+  if (pos) std::memcpy(pos, hp.data(), (size_t)n * 24);
+  if (quat) std::memcpy(quat, hp.data() + (size_t)n * 3, (size_t)n * 32);
+  if (lin) std::memcpy(lin, hp.data() + (size_t)n * 7, (size_t)n * 24);
+  if (ang) std::memcpy(ang, hp.data() + (size_t)n * 10, (size_t)n * 24);
+  if (latch) std::memcpy(latch, hl.data(), (size_t)n);
   return VX_OK;
 }
 
@@ -1058,16 +1162,17 @@ int64_t vx_contact_pairs(vx_lattice* h, int64_t* pairs, int64_t cap) {
   if (!h) return -1;
   if (!h->collide() || h->tables_dirty || !h->rowptr.p) return 0;
   if (cudaSetDevice(h->device) != cudaSuccess) return -1;
+  const Slab& sl = h->slabs[0];
   const int S = (int)h->surf_local.size();
   std::vector<int> rp(S + 1);
   if (cudaMemcpy(rp.data(), h->rowptr.p, (size_t)(S + 1) * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   const long long tot = std::min<long long>(rp[S], h->cap);
   std::vector<int> col((size_t)std::max<long long>(tot, 1));
   if (tot && cudaMemcpy(col.data(), h->col.p, (size_t)tot * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  std::vector<long long> eol(h->nloc, -1);
+  std::vector<long long> eol(sl.nloc, -1);
   for (long long e = 0; e < h->N; ++e) {
-    const long long li = h->box_of_ext[e] - h->box_base;
-    if (li >= 0 && li < (long long)h->nloc) eol[li] = e;
+    const long long li = h->box_of_ext[e] - sl.box_base;
+    if (li >= 0 && li < (long long)sl.nloc) eol[li] = e;
   }
   std::vector<std::pair<long long, long long>> out;
   for (int s = 0; s < S; ++s) {

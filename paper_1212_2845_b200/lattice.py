@@ -44,6 +44,14 @@ class State:
     latch: np.ndarray    # (n,) uint8
 
 
+def slab_planes(nx, nranks, rank):
+    """(x_begin, x_end) of rank's x-slab (vx_slab_planes; host-only)."""
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    _check(N.load().vx_slab_planes(int(nx), int(nranks), int(rank), ctypes.byref(a),
+                                   ctypes.byref(b)))
+    return a.value, b.value
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(N.load().vx_nccl_unique_id(buf))

@@ -1,0 +1,75 @@
+"""x-slab decomposition on one GPU: P slabs emulated inside one
+handle (ghost planes by device copies, the same slab arithmetic the NCCL
+ranks run) must reproduce the single-domain run bit for bit."""
+import numpy as np
+import pytest
+
+import workloads as W
+from paper_1212_2845_b200 import from_scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _flat(st):
+    return np.concatenate([st.pos.ravel(), st.quat.ravel(), st.linmom.ravel(),
+                           st.angmom.ravel(), st.latch.astype(float)])
+
+
+def _scenes():
+    b = W.block(23, 12, 10)
+    b.env["zeta_ground"] = 0.0
+    w = W.walker(16, 8, 8)
+    w.env["T_freq"] = 1000.0
+    c = W.cube(contact_variant=True, n=6)
+    rng = np.random.default_rng(3)
+    pos, quat, P, phi, latch = c.initial_state()
+    P = P + rng.normal(size=P.shape) * 1e-10
+    c.initial_state = (lambda s=(pos, quat, P, phi, latch): s)
+    return {"block": b, "walker": w, "cube": c, "cantilever": W.cantilever()}
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("name", ["block", "walker", "cube", "cantilever"])
+def test_slabs_bitwise_equal_single_domain(name, prec):
+    sc = _scenes()[name]
+    ref = from_scene(sc, precision=prec)
+    ref.step(150)
+    r = _flat(ref.read_state())
+    nx = sc.cells.shape[2]
+    for P in sorted({2, 3, 4, 5, 7, min(8, nx)}):
+        lat = from_scene(sc, precision=prec, nranks=P)
+        assert lat.launches_per_step == 1 + 2 * P
+        lat.step(150)
+        assert np.array_equal(_flat(lat.read_state()), r), (name, prec, P)
+        lat.destroy()
+
+
+def test_slabs_read_voxels_and_checkpoint():
+    sc = W.block(23, 12, 10)
+    lat = from_scene(sc, precision=32, nranks=4)
+    lat.step(40)
+    ids = np.array([0, 5, 600, 1500, sc.num_voxels - 1])
+    v = lat.read_voxels(ids)
+    full = lat.read_state()
+    assert np.array_equal(v.pos, full.pos[ids]) and np.array_equal(v.quat, full.quat[ids])
+    blob = lat.save_checkpoint()
+    lat.step(30)
+    after = _flat(lat.read_state())
+    lat2 = from_scene(sc, precision=32, nranks=4)
+    lat2.load_checkpoint(blob)
+    lat2.step(30)
+    assert np.array_equal(_flat(lat2.read_state()), after)
+
+
+def test_slabs_divergence_and_rejections():
+    from paper_1212_2845_b200 import DivergedError, VoxError
+    sc = W.cantilever()
+    lat = from_scene(sc, precision=64, nranks=3)
+    pos, quat, P, phi, latch = sc.initial_state()
+    P[7, 2] = np.inf
+    lat.set_state(pos, quat, P, phi, latch)
+    with pytest.raises(DivergedError, match="voxel 6 at step 0"):
+        lat.step(3)
+    s3 = W.hollow_sphere(n=14, r_in=4, r_out=7)
+    with pytest.raises(VoxError):
+        from_scene(s3, precision=32, nranks=2)        # self collision needs one slab

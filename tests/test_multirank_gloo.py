@@ -1,0 +1,86 @@
+"""The N>1 path's host logic on CPU with world_size-2 (and 3) gloo process
+groups: NCCL-id bootstrap, slab partition, the ghost-plane protocol (with gloo
+send/recv standing in for NCCL) and the max-over-ranks timing reduction."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch
+    from paper_1212_2845_b200 import dist as vd
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    # 1. NCCL bootstrap id: identical bytes on every rank
+    nid = vd.bootstrap_nccl_id(dist, rank)
+    ids = [None] * world
+    dist.all_gather_object(ids, nid)
+    out["ids_equal"] = all(x == ids[0] for x in ids) and len(ids[0]) == 128
+    # 2. slab partition of a 37-plane lattice tiles [0, nx) exactly
+    nx, ny, nz = 37, 3, 4
+    x0, x1, xl0, xl1 = vd.ghost_planes(nx, world, rank)
+    sl = [None] * world
+    dist.all_gather_object(sl, (x0, x1))
+    out["slabs"] = sl
+    # 3. ghost-plane protocol on a box-ordered (x slowest) field, gloo for NCCL
+    rng = np.random.default_rng(0)
+    glob = rng.normal(size=(nx, ny, nz))
+    local = np.zeros((xl1 - xl0, ny, nz))
+    local[x0 - xl0:x1 - xl0] = glob[x0:x1]
+    reqs = []
+    bufs = {}
+    if x0 > 0:
+        reqs.append(dist.isend(torch.from_numpy(local[x0 - xl0].copy()), rank - 1))
+        bufs["L"] = torch.zeros(ny, nz, dtype=torch.float64)
+        reqs.append(dist.irecv(bufs["L"], rank - 1))
+    if x1 < nx:
+        reqs.append(dist.isend(torch.from_numpy(local[x1 - 1 - xl0].copy()), rank + 1))
+        bufs["R"] = torch.zeros(ny, nz, dtype=torch.float64)
+        reqs.append(dist.irecv(bufs["R"], rank + 1))
+    for r in reqs:
+        r.wait()
+    if "L" in bufs:
+        local[0] = bufs["L"].numpy()
+    if "R" in bufs:
+        local[-1] = bufs["R"].numpy()
+    out["ghosts_ok"] = bool(np.array_equal(local, glob[xl0:xl1]))
+    # 4. max over ranks of per-rank times
+    out["max"] = vd.max_over_ranks([1.0 + rank, 10.0 - rank], dist)
+    dist.destroy_process_group()
+    q.put((rank, out))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_host_logic_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    slabs = res[0]["slabs"]
+    assert slabs[0][0] == 0 and slabs[-1][1] == 37
+    assert all(slabs[i][1] == slabs[i + 1][0] for i in range(world - 1))
+    sizes = [b - a for a, b in slabs]
+    assert max(sizes) - min(sizes) <= 1
+    for r in range(world):
+        assert res[r]["ids_equal"] and res[r]["ghosts_ok"]
+        assert res[r]["max"] == [float(world), 10.0]
