@@ -38,9 +38,26 @@ UNIT = "voxel-steps/s"
 
 # Algorithmic HBM bytes per voxel-step, fp32 / fp64
 ALG_BYTES = {
-    32: {"bonds": 56 + 108, "integrate": 108 + 56 + 56},
-    64: {"bonds": 112 + 216, "integrate": 216 + 112 + 112},
+    32: {"bonds": 56 + 108, "integrate": 108 + 56 + 56, "fused": 56 + 56},
+    64: {"bonds": 112 + 216, "integrate": 216 + 112 + 112, "fused": 112 + 112},
 }
+# FP32 (FP64) lane-operations per voxel-step of the fused kernel, counted by ncu
+# (sass thread-instructions of the FADD/FMUL/FFMA/MUFU pipes, FFMA counted once;
+# profiles/); None until measured.
+ALU_OPS_PER_VOXEL = {32: None, 64: None}
+
+
+def alu_roof(prec, ms, voxels, clocks):
+    ops = ALU_OPS_PER_VOXEL.get(prec)
+    if not ops:
+        return None
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    lanes = 148 * 128 if prec == 32 else 148 * 64
+    peak = lanes * mhz * 1e6 / 1e12                    # Tops/s (1 op / lane / clock)
+    achieved = ops * voxels / (ms / 1e3) / 1e12
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+            "frac": achieved / peak, "ops_per_voxel": ops,
+            "peak_note": f"148 SMs x {lanes // 148} lanes x {mhz:.0f} MHz (median SM clock)"}
 
 
 def _peaks():
@@ -195,7 +212,7 @@ def run_ours(args):
 
     sc = scene_for(args.config, args.precision)
     lat = from_scene(sc, precision=args.precision, device=local, rank=rank, nranks=world,
-                     nccl_id=nid, init_state=sc.v0 is not None)
+                     nccl_id=nid, init_state=sc.v0 is not None, engine=args.engine)
     N = lat.num_voxels
     stream = torch.cuda.ExternalStream(lat.stream, device=torch.device("cuda", local))
 
@@ -231,31 +248,35 @@ def run_ours(args):
     x0, x1 = lat.owned_planes()
     vox_rank = N * (x1 - x0) / sc.cells.shape[2]   # dense boxes: voxels per rank
     alg = ALG_BYTES[args.precision]
-    avg = {k: kt[k][0] / max(kt[k][1], 1) for k in ("bonds", "integrate")}
-    # bonds is launched once per step at N=1 (3x with the halo split)
-    per_step_ms = {k: kt[k][0] / args.steps for k in ("bonds", "integrate")}
+    fused = lat.engine == "fused"
+    kinds = ("fused",) if fused else ("bonds", "integrate")
+    slot = {"fused": "integrate", "bonds": "bonds", "integrate": "integrate"}
+    avg = {k: kt[slot[k]][0] / max(kt[slot[k]][1], 1) for k in kinds}
+    per_step_ms = {k: kt[slot[k]][0] / args.steps for k in kinds}
     dom = max(per_step_ms, key=per_step_ms.get)
     peak, peak_src = _peaks()
-    achieved = alg[dom] * vox_rank / (per_step_ms[dom] / 1e3) / 1e9
+    gbps = {k: alg[k] * vox_rank / (per_step_ms[k] / 1e3) / 1e9 for k in kinds}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
             tr = json.load(open(tp))
-            key = f"{args.config}:fp{args.precision}:{dom}"
-            traffic = tr.get(key)
+            t = tr.get(f"{args.config}:fp{args.precision}:{dom}")
+            traffic = t / (1e-3 * per_step_ms[dom]) / 1e9 if t else None   # ncu bytes -> GB/s
+            traffic = {"bytes_per_launch": t, "GBps_at_live_time": traffic} if t else None
         except Exception:
             traffic = None
-    roof = {"bound": "hbm", "kernel": "k_bonds (K3)" if dom == "bonds" else "k_integrate (K4)",
-            "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic,
-            "alg_bytes_per_voxel": alg[dom],
-            "avg_launch_ms": avg[dom],
-            "kernels": {k: {"ms_per_step": per_step_ms[k],
-                            "GBps": alg[k] * vox_rank / (per_step_ms[k] / 1e3) / 1e9}
-                        for k in ("bonds", "integrate")},
-            "step_GBps_alg": (alg["bonds"] + alg["integrate"]) * N
-            / (ms_max / args.steps / 1e3) / 1e9}
+    names = {"bonds": "k_bonds (K3)", "integrate": "k_integrate (K4)",
+             "fused": "k_step_fused (K3+K4 single pass)"}
+    roof = {"bound": "hbm", "kernel": names[dom],
+            "achieved": gbps[dom], "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+            "frac": gbps[dom] / peak, "traffic": traffic,
+            "alg_bytes_per_voxel": alg[dom], "avg_launch_ms": avg[dom],
+            "kernels": {k: {"ms_per_step": per_step_ms[k], "GBps": gbps[k]} for k in kinds},
+            "step_GBps_alg": sum(alg[k] for k in kinds) * N / (ms_max / args.steps / 1e3) / 1e9}
+    if fused:
+        # compute side of the single pass: FP32 lanes x clock
+        roof["alu"] = alu_roof(args.precision, per_step_ms[dom], vox_rank, clocks)
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
@@ -324,6 +345,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C5")
     ap.add_argument("--precision", type=int, default=32)
+    ap.add_argument("--engine", default="fused", choices=["fused", "two_pass"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

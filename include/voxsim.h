@@ -207,6 +207,18 @@ vx_status vx_kernel_times(vx_lattice* h, double out_ms[4], int64_t counts[4]);
 /* Number of kernels vx_step launches per step with the current settings. */
 int32_t vx_launches_per_step(const vx_lattice* h);
 
+/* Step engine.  VX_ENGINE_TWO_PASS: the bond kernel K3 writes per-bond load
+ * records to HBM and the gather-integrate kernel K4 reads them ("forces
+ * … calculated separately, then … summed"; 384 B/voxel-step in fp32).
+ * VX_ENGINE_FUSED: one kernel per step sweeps x-planes, keeps every bond's
+ * loads on chip and writes S_{n+1} to a second state copy (112 B/voxel-step);
+ * same arithmetic per bond and per voxel, same summation order.  Needs
+ * nz <= 256 (INVALID_ARG otherwise).  In kernel timing (vx_kernel_times) the
+ * fused kernel is reported in slot [1]. */
+typedef enum { VX_ENGINE_TWO_PASS = 0, VX_ENGINE_FUSED = 1 } vx_engine;
+vx_status vx_set_engine(vx_lattice* h, int32_t engine);
+int32_t vx_get_engine(const vx_lattice* h);
+
 /* Release all device memory and the communicator. NULL is a no-op. */
 void vx_destroy(vx_lattice* h);
 

@@ -81,6 +81,8 @@ SIGNATURES = {
     "vx_set_instrumentation": (_I32, [_P, _I32]),
     "vx_kernel_times": (_I32, [_P, _DP, ctypes.POINTER(_I64)]),
     "vx_launches_per_step": (_I32, [_P]),
+    "vx_set_engine": (_I32, [_P, _I32]),
+    "vx_get_engine": (_I32, [_P]),
     "vx_destroy": (None, [_P]),
     "vx_last_error": (ctypes.c_char_p, []),
     "vx_nccl_unique_id": (_I32, [_P]),

@@ -89,8 +89,19 @@ struct Slab {
   int x0 = 0, x1 = 0, xl0 = 0, xl1 = 0;
   uint32_t nloc = 0;
   long long box_base = 0;              // xl0 * plane
-  DevBuf pos, quat, mom, ang, recA, recB, recC, fextd, cf, meta_d, ext_of_local;
+  DevBuf buf[2][4];                    // state, double-buffered: [parity][pos, quat, mom, ang]
+  int par = 0;                         // which copy holds the current state S_n
+  DevBuf recA, recB, recC, fextd, cf, meta_d, ext_of_local;
   std::vector<uint32_t> meta_static;   // static meta bits, local box order
+  DevBuf& pos() { return buf[par][0]; }
+  DevBuf& quat() { return buf[par][1]; }
+  DevBuf& mom() { return buf[par][2]; }
+  DevBuf& ang() { return buf[par][3]; }
+  const DevBuf& pos() const { return buf[par][0]; }
+  const DevBuf& quat() const { return buf[par][1]; }
+  const DevBuf& mom() const { return buf[par][2]; }
+  const DevBuf& ang() const { return buf[par][3]; }
+  const DevBuf& out(int a) const { return buf[par ^ 1][a]; }   // S_{n+1} of the fused step
 };
 
 }  // namespace
@@ -142,6 +153,14 @@ struct vx_lattice {
   ncclComm_t comm = nullptr;
   long long steps_done = 0;
 
+  int engine = VX_ENGINE_TWO_PASS;
+  bool fused_smem_set[2] = {false, false};
+
+  bool fused() const { return engine == VX_ENGINE_FUSED; }
+  bool fused_supported() const { return nz <= 256; }
+  void flip() {
+    for (auto& s : slabs) s.par ^= 1;
+  }
   bool nccl() const { return nranks > 1 && !emulated; }
   bool collide() const { return env_set && env.self_collision && nsurf > 0; }
   int bond_launches() const {
@@ -149,7 +168,8 @@ struct vx_lattice {
     return nranks > 1 ? 3 : 1;
   }
   int launches_per_step() const {
-    int k = 1 + bond_launches() + (int)slabs.size();  // clock, bonds, integrate
+    int k = 1 + (int)slabs.size();                     // clock, integrate or fused
+    if (!fused()) k += bond_launches();                // bonds
     if (collide()) k += 2;
     return k;
   }
@@ -216,10 +236,10 @@ vx_status build_topology(vx_lattice* h) {
 
 template <class R> Dev<R> make_dev(const vx_lattice* h, const Slab& s) {
   Dev<R> d;
-  d.pos = s.pos.as<typename VT<R>::R4>();
-  d.quat = s.quat.as<typename VT<R>::R4>();
-  d.mom = s.mom.as<typename VT<R>::R4>();
-  d.ang = s.ang.as<typename VT<R>::R2>();
+  d.pos = s.pos().as<typename VT<R>::R4>();
+  d.quat = s.quat().as<typename VT<R>::R4>();
+  d.mom = s.mom().as<typename VT<R>::R4>();
+  d.ang = s.ang().as<typename VT<R>::R2>();
   d.recA = s.recA.as<typename VT<R>::R4>();
   d.recB = s.recB.as<typename VT<R>::R4>();
   d.recC = s.recC.as<R>();
@@ -330,7 +350,7 @@ template <class R> vx_status upload_tables(vx_lattice* h) {
     c.mu_s = (R)m.mu_s;
     c.mu_d = (R)m.mu_d;
     c.kc = (R)(m.E * l);
-    c.pad = (R)0;
+    c.pad0 = c.pad1 = (R)0;
   }
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) {
@@ -342,6 +362,9 @@ template <class R> vx_status upload_tables(vx_lattice* h) {
       const double mmin = std::min(md[i].m, md[j].m), Imin = std::min(md[i].I, md[j].I);
       p.ct = (R)(2 * e.zeta_bond * std::sqrt(mmin * a1));   // Eq. 34, R10
       p.cr = (R)(2 * e.zeta_bond * std::sqrt(Imin * a2));   // Eq. 35, R11
+      p.inv_m_b = (R)(1.0 / md[j].m);
+      p.inv_I_b = (R)(1.0 / md[j].I);
+      p.pad0 = p.pad1 = (R)0;
     }
   VX_TRY(h->mat.alloc(mc.size() * sizeof(MatC<R>)));
   VX_TRY(h->pair.alloc(pc.size() * sizeof(PairC<R>)));
@@ -374,7 +397,7 @@ template <class R> vx_status compute_dt(vx_lattice* h) {
     // planes [xl0, x1): the right ghost plane's +x bonds belong to the next slab
     // (its +x neighbour is outside this slab's box)
     const uint32_t end = (uint32_t)(s.x1 - s.xl0) * h->plane;
-    k_dt<R><<<grid_of(end), 256, 0, h->stream>>>(s.pos.as<typename VT<R>::R4>(), 0u, end,
+    k_dt<R><<<grid_of(end), 256, 0, h->stream>>>(s.pos().as<typename VT<R>::R4>(), 0u, end,
                                                  h->plane, (uint32_t)h->nz, h->pair_w2.as<double>(),
                                                  h->mat_w2.as<double>(), n, c);
   }
@@ -462,6 +485,39 @@ template <class R> void launch_integrate(vx_lattice* h, const Slab& s, const Dev
     k_integrate<R, false><<<grid_of(end - beg), 256, 0, h->stream>>>(d, beg, end, s.ext_of_local.as<uint32_t>());
 }
 
+// Fused single pass over a slab's owned planes: S_n (current copy) -> S_{n+1}
+// (other copy).  Block = one thread per z (nz <= 256) x TY rows x SX planes.
+template <class R> vx_status launch_fused(vx_lattice* h, const Slab& s, bool col) {
+  const Dev<R> d = make_dev<R>(h, s);
+  FusedArgs<R> a;
+  a.opos = s.out(0).as<typename VT<R>::R4>();
+  a.oquat = s.out(1).as<typename VT<R>::R4>();
+  a.omom = s.out(2).as<typename VT<R>::R4>();
+  a.oang = s.out(3).as<typename VT<R>::R2>();
+  a.ext_of_local = s.ext_of_local.as<uint32_t>();
+  a.ty = std::min(8, h->ny);
+  a.ntiles_y = (h->ny + a.ty - 1) / a.ty;
+  a.p0 = s.x0 - s.xl0;
+  a.p1 = s.x1 - s.xl0;
+  const int planes = a.p1 - a.p0;
+  const int target = 148 * 8;   // blocks: ~4 waves at 2 resident blocks per SM
+  const int nseg = std::max(1, std::min(planes, (target + a.ntiles_y - 1) / a.ntiles_y));
+  a.sx = (planes + nseg - 1) / nseg;
+  const int segs = (planes + a.sx - 1) / a.sx;
+  const int threads = ((h->nz + 31) / 32) * 32;
+  const size_t smem = fused_smem<R>(a.ty, threads);
+  const int pi = sizeof(R) == 4 ? 0 : 1;
+  if (!h->fused_smem_set[pi]) {
+    VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    h->fused_smem_set[pi] = true;
+  }
+  const unsigned grid = (unsigned)(a.ntiles_y * segs);
+  if (col) k_step_fused<R, true><<<grid, threads, smem, h->stream>>>(d, a);
+  else k_step_fused<R, false><<<grid, threads, smem, h->stream>>>(d, a);
+  return VX_OK;
+}
+
 // The four SoA state arrays of a slab, with element sizes.
 struct Arr {
   char* base;
@@ -469,10 +525,10 @@ struct Arr {
 };
 void state_arrays(const vx_lattice* h, const Slab& s, Arr out[4]) {
   const size_t r = rsize(h->prec);
-  out[0] = {s.pos.as<char>(), 4 * r};
-  out[1] = {s.quat.as<char>(), 4 * r};
-  out[2] = {s.mom.as<char>(), 4 * r};
-  out[3] = {s.ang.as<char>(), 2 * r};
+  out[0] = {s.pos().as<char>(), 4 * r};
+  out[1] = {s.quat().as<char>(), 4 * r};
+  out[2] = {s.mom().as<char>(), 4 * r};
+  out[3] = {s.ang().as<char>(), 2 * r};
 }
 inline char* plane_ptr(const Arr& a, const Slab& s, int x, size_t plane) {
   return a.base + (size_t)(x - s.xl0) * plane * a.esz;
@@ -541,6 +597,21 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
   }
   if (h->emulated) VX_TRY(halo_local(h));
   if (ev) VX_CUDA(cudaEventRecord(ev[1], h->stream));
+  if (h->fused()) {
+    if (h->nccl()) {   // ghost planes of S_n before the single pass
+      VX_CUDA(cudaEventRecord(h->ev_k4, h->stream));
+      VX_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_k4, 0));
+      VX_TRY(halo_nccl(h));
+      VX_CUDA(cudaEventRecord(h->ev_halo, h->comm_stream));
+      VX_CUDA(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+    }
+    if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
+    for (const Slab& s : h->slabs) VX_TRY(launch_fused<R>(h, s, col));
+    if (ev) VX_CUDA(cudaEventRecord(ev[3], h->stream));
+    VX_CUDA(cudaGetLastError());
+    h->flip();
+    return VX_OK;
+  }
   if (h->nccl()) {
     // halo of S_n on the comm stream, overlapped with the interior bonds
     const Slab& s = h->slabs[0];
@@ -581,33 +652,39 @@ template <class R> vx_status run_steps(vx_lattice* h, long long n) {
       VX_CUDA(cudaEventElapsedTime(&c, e[0], e[1]));
       VX_CUDA(cudaEventElapsedTime(&t, e[0], e[3]));
       h->t_ms[0] += a; h->t_ms[1] += b; h->t_ms[2] += c; h->t_ms[3] += t;
-      h->t_cnt[0] += h->bond_launches();
+      h->t_cnt[0] += h->fused() ? 0 : h->bond_launches();
       h->t_cnt[1] += (long long)h->slabs.size();
       h->t_cnt[2] += h->collide() ? 3 : 1;
       h->t_cnt[3] += h->launches_per_step();
     }
     return VX_OK;
   }
-  // CUDA graphs of G steps; the remainder is captured as its own graph
+  // CUDA graphs of G steps; the remainder is captured as its own graph.  The
+  // fused engine ping-pongs two state copies, so a graph also depends on which
+  // copy is current when it starts (key = 2 g + parity).
   const long long G = 32;
   long long left = n;
   while (left > 0) {
     const long long g = left >= G ? G : left;
-    auto it = h->graphs.find(g);
+    const int par = h->slabs[0].par;
+    const long long key = 2 * g + (h->fused() ? par : 0);
+    auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {
       cudaGraph_t graph;
       VX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
       vx_status st = VX_OK;
       for (long long s = 0; s < g && st == VX_OK; ++s) st = enqueue_step<R>(h, nullptr);
       cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+      for (auto& s : h->slabs) s.par = par;   // capture only recorded the flips
       if (st != VX_OK) return st;
       if (ce != cudaSuccess) return fail(VX_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
       cudaGraphExec_t ex;
       VX_CUDA(cudaGraphInstantiate(&ex, graph, 0));
       cudaGraphDestroy(graph);
-      it = h->graphs.emplace(g, ex).first;
+      it = h->graphs.emplace(key, ex).first;
     }
     VX_CUDA(cudaGraphLaunch(it->second, h->stream));
+    if (h->fused() && (g & 1)) h->flip();
     left -= g;
   }
   VX_CUDA(cudaStreamSynchronize(h->stream));
@@ -626,6 +703,20 @@ vx_status check_device() {
 
 vx_status set_device(const vx_lattice* h) {
   VX_CUDA(cudaSetDevice(h->device));
+  return VX_OK;
+}
+
+// Copy the current state into the fused engine's second buffer (allocated on
+// first use); needed before fused steps after any host-side state change.
+vx_status sync_state_copies(vx_lattice* h) {
+  for (Slab& s : h->slabs)
+    for (int a = 0; a < 4; ++a) {
+      const DevBuf& c = s.buf[s.par][a];
+      DevBuf& o = s.buf[s.par ^ 1][a];
+      VX_TRY(o.alloc(c.bytes));
+      VX_CUDA(cudaMemcpyAsync(o.p, c.p, c.bytes, cudaMemcpyDeviceToDevice, h->stream));
+    }
+  VX_CUDA(cudaStreamSynchronize(h->stream));
   return VX_OK;
 }
 
@@ -744,17 +835,17 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
     return bail(s);
   for (Slab& sl : h->slabs) {
     const size_t n = sl.nloc;
-    if ((s = sl.pos.alloc(n * 4 * r)) || (s = sl.quat.alloc(n * 4 * r)) || (s = sl.mom.alloc(n * 4 * r)) ||
-        (s = sl.ang.alloc(n * 2 * r)) || (s = sl.recA.alloc(3 * n * 4 * r)) ||
+    if ((s = sl.pos().alloc(n * 4 * r)) || (s = sl.quat().alloc(n * 4 * r)) || (s = sl.mom().alloc(n * 4 * r)) ||
+        (s = sl.ang().alloc(n * 2 * r)) || (s = sl.recA.alloc(3 * n * 4 * r)) ||
         (s = sl.recB.alloc(3 * n * 4 * r)) || (s = sl.recC.alloc(3 * n * r)) ||
         (s = sl.meta_d.alloc(n * 4)) || (s = sl.ext_of_local.alloc(n * 4)))
       return bail(s);
     // initial state: at rest on the lattice sites, identity orientation (.w = 1)
-    if (cudaMemset(sl.pos.p, 0, sl.pos.bytes) != cudaSuccess || cudaMemset(sl.mom.p, 0, sl.mom.bytes) != cudaSuccess ||
-        cudaMemset(sl.ang.p, 0, sl.ang.bytes) != cudaSuccess || cudaMemset(sl.recA.p, 0, sl.recA.bytes) != cudaSuccess ||
+    if (cudaMemset(sl.pos().p, 0, sl.pos().bytes) != cudaSuccess || cudaMemset(sl.mom().p, 0, sl.mom().bytes) != cudaSuccess ||
+        cudaMemset(sl.ang().p, 0, sl.ang().bytes) != cudaSuccess || cudaMemset(sl.recA.p, 0, sl.recA.bytes) != cudaSuccess ||
         cudaMemset(sl.recB.p, 0, sl.recB.bytes) != cudaSuccess || cudaMemset(sl.recC.p, 0, sl.recC.bytes) != cudaSuccess)
       return bail(fail(VX_ERR_CUDA, "memset failed"));
-    std::vector<char> q(sl.quat.bytes, 0);
+    std::vector<char> q(sl.quat().bytes, 0);
     for (size_t i = 0; i < n; ++i) {
       if (r == 4) { float one = 1.f; std::memcpy(&q[i * 16 + 12], &one, 4); }
       else { double one = 1.0; std::memcpy(&q[i * 32 + 24], &one, 8); }
@@ -764,10 +855,11 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
       const long long li = h->box_of_ext[e] - sl.box_base;
       if (li >= 0 && li < (long long)n) eol[li] = (uint32_t)e;
     }
-    if (cudaMemcpy(sl.quat.p, q.data(), q.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+    if (cudaMemcpy(sl.quat().p, q.data(), q.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(sl.ext_of_local.p, eol.data(), n * 4, cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(VX_ERR_CUDA, "upload failed"));
   }
+  if ((s = sync_state_copies(h)) != VX_OK) return bail(s);
   Clock c0{};
   c0.err = ~0ULL;
   c0.force_rebuild = 1;
@@ -951,7 +1043,7 @@ int64_t ckpt_nloc(const vx_lattice* h) {
 int64_t vx_checkpoint_bytes(const vx_lattice* h) {
   if (!h) return -1;
   int64_t b = sizeof(CkptHeader) + sizeof(Clock);
-  for (const Slab& s : h->slabs) b += (int64_t)(s.pos.bytes + s.quat.bytes + s.mom.bytes + s.ang.bytes);
+  for (const Slab& s : h->slabs) b += (int64_t)(s.pos().bytes + s.quat().bytes + s.mom().bytes + s.ang().bytes);
   return b;
 }
 
@@ -963,7 +1055,7 @@ vx_status vx_save_checkpoint(vx_lattice* h, void* buf, int64_t bytes) {
   std::memcpy(p, &hd, sizeof hd);
   p += sizeof hd;
   for (Slab& s : h->slabs)
-    for (DevBuf* b : {&s.pos, &s.quat, &s.mom, &s.ang}) {
+    for (DevBuf* b : {&s.pos(), &s.quat(), &s.mom(), &s.ang()}) {
       VX_CUDA(cudaMemcpy(p, b->p, b->bytes, cudaMemcpyDeviceToHost));
       p += b->bytes;
     }
@@ -982,7 +1074,7 @@ vx_status vx_load_checkpoint(vx_lattice* h, const void* buf, int64_t bytes) {
     return fail(VX_ERR_INVALID_ARG, "checkpoint does not match this lattice (shape, precision or rank)");
   p += sizeof hd;
   for (Slab& s : h->slabs)
-    for (DevBuf* b : {&s.pos, &s.quat, &s.mom, &s.ang}) {
+    for (DevBuf* b : {&s.pos(), &s.quat(), &s.mom(), &s.ang()}) {
       VX_CUDA(cudaMemcpy(b->p, p, b->bytes, cudaMemcpyHostToDevice));
       p += b->bytes;
     }
@@ -1205,5 +1297,17 @@ vx_status vx_kernel_times(vx_lattice* h, double out_ms[4], int64_t counts[4]) {
   return VX_OK;
 }
 int32_t vx_launches_per_step(const vx_lattice* h) { return h ? h->launches_per_step() : -1; }
+
+vx_status vx_set_engine(vx_lattice* h, int32_t engine) {
+  if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
+  if (engine != VX_ENGINE_TWO_PASS && engine != VX_ENGINE_FUSED)
+    return fail(VX_ERR_INVALID_ARG, "unknown engine");
+  if (engine == VX_ENGINE_FUSED && !h->fused_supported())
+    return fail(VX_ERR_INVALID_ARG, "the fused engine needs nz <= 256");
+  h->engine = engine;
+  h->clear_graphs();
+  return VX_OK;
+}
+int32_t vx_get_engine(const vx_lattice* h) { return h ? h->engine : -1; }
 
 }  // extern "C"

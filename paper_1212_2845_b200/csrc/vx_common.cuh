@@ -56,20 +56,23 @@ __device__ __forceinline__ unsigned long long rbits(double x) {
 }
 
 // Per-material constants (host fp64, cast to R).
-template <class R> struct MatC {
+// (16-byte aligned, multiples of 4 scalars: loaded as 128-bit vectors)
+template <class R> struct __align__(16) MatC {
   R m, inv_m, inv_I, dt_m, dt_I;  // dt_m = dt/m, dt_I = dt/I
   R mg;                           // m * g
   R cgt, cgr;                     // ground damping 2 zeta_g sqrt(m E l), 2 zeta_g sqrt(I G l^3/6)
   R kf, cfl;                      // floor stiffness E l and damping 2 zeta_col sqrt(m kf)
   R alpha, mu_s, mu_d;
   R kc;                           // contact stiffness E l
-  R pad;
+  R pad0, pad1;
 };
-// Per material-pair constants (Eq. 1-12, 34-35, 40).
-template <class R> struct PairC {
+// Per ordered material-pair (a, b) constants (Eq. 1-12, 34-35, 40).
+template <class R> struct __align__(16) PairC {
   R a1, a2, b1, b2, b3;
   R alpha_mean;                   // (alpha_1 + alpha_2) / 2
   R ct, cr;                       // 2 zeta_b sqrt(m_min a1), 2 zeta_b sqrt(I_min a2)
+  R inv_m_b, inv_I_b;             // 1/m, 1/I of material b (damping velocities)
+  R pad0, pad1;
 };
 
 // ---------------------------------------------------------------- vec3

@@ -155,23 +155,36 @@ template <class R> __device__ __forceinline__ R rotvec_scale(R w, R x, R y, R z)
   return R(2) * vx_atan2(s, w) / s;
 }
 
-// Voxel a = id (negative side, R4), b = id + stride(AX).  Loads in the frame
-// of a, Eq. 13-24 sign-fixed and negated (R1, R3), back to world
-// (P:206), plus local damping (Eq. 33-35, R10, R11).
+// Voxel a (negative side, R4) and b = a + e_AX.  Loads in the frame of a
+// (P:189), Eq. 13-24 sign-fixed and negated (R1, R3), back to world,
+// plus local damping (Eq. 33-35, R10, R11).  Shared by K3 and the fused step.
+template <class R> struct VS {   // one voxel's state as loaded
+  typename VT<R>::R4 p, q, mo;   // (u, meta), quaternion (x,y,z,w), (P, phi.x)
+  typename VT<R>::R2 an;         // (phi.y, phi.z)
+};
+template <class R>
+__device__ __forceinline__ VS<R> ld_vs(const typename VT<R>::R4* __restrict__ pos,
+                                       const typename VT<R>::R4* __restrict__ quat,
+                                       const typename VT<R>::R4* __restrict__ mom,
+                                       const typename VT<R>::R2* __restrict__ ang, uint32_t i) {
+  VS<R> s;
+  s.p = pos[i];
+  s.q = quat[i];
+  s.mo = mom[i];
+  s.an = ang[i];
+  return s;
+}
+
 template <int AX, class R>
-__device__ __forceinline__ void bond_one(const Dev<R>& d, uint32_t ia, uint32_t ib,
-                                         const Rot<R>& Ra, const typename VT<R>::R4& qa,
-                                         V3<R> ua, V3<R> Va, V3<R> wa, int mat_a, R dT) {
+__device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
+                                          const typename VT<R>::R4& qa, V3<R> ua, V3<R> Va,
+                                          V3<R> wa, int mat_a, const VS<R>& b, R dT, V3<R>& Fa,
+                                          V3<R>& Ma, V3<R>& Mbw) {
   using R4 = typename VT<R>::R4;
-  using R2 = typename VT<R>::R2;
-  const R4 pb = d.pos[ib];
-  const R4 qb = d.quat[ib];
-  const R4 mob = d.mom[ib];
-  const R2 anb = d.ang[ib];
-  const uint32_t mb_meta = meta_of(pb.w);
-  const int mat_b = mb_meta & M_MAT;
+  const R4& pb = b.p;
+  const R4& qb = b.q;
+  const int mat_b = meta_of(pb.w) & M_MAT;
   const PairC<R> c = d.pair[mat_a * d.nmat + mat_b];
-  const MatC<R>& Mb = d.mat[mat_b];
   const R l = d.l;
 
   // relative position in a's frame, cancellation-free:
@@ -198,13 +211,13 @@ __device__ __forceinline__ void bond_one(const Dev<R>& d, uint32_t ia, uint32_t 
   const V3<R> ma = mk(c.a2 * th.x, -c.b2 * Z2 - c.b3 * th.y, c.b2 * Y2 - c.b3 * th.z);
   const V3<R> mbl = mk(-c.a2 * th.x, -c.b2 * Z2 - R(2) * c.b3 * th.y,
                        c.b2 * Y2 - R(2) * c.b3 * th.z);
-  V3<R> Fa = mul(Ra, to_world<AX>(fa));
-  V3<R> Ma = mul(Ra, to_world<AX>(ma));
-  V3<R> Mbw = mul(Ra, to_world<AX>(mbl));
+  Fa = mul(Ra, to_world<AX>(fa));
+  Ma = mul(Ra, to_world<AX>(ma));
+  Mbw = mul(Ra, to_world<AX>(mbl));
 
   // Eq. 33-35 in the world frame
-  const V3<R> Vb = Mb.inv_m * mk(mob.x, mob.y, mob.z);
-  const V3<R> wb = Mb.inv_I * mk(mob.w, anb.x, anb.y);
+  const V3<R> Vb = c.inv_m_b * mk(b.mo.x, b.mo.y, b.mo.z);
+  const V3<R> wb = c.inv_I_b * mk(b.mo.w, b.an.x, b.an.y);
   const V3<R> Vavg = R(0.5) * (Va + Vb);
   const V3<R> wavg = R(0.5) * (wa + wb);
   V3<R> r = du;
@@ -216,54 +229,221 @@ __device__ __forceinline__ void bond_one(const Dev<R>& d, uint32_t ia, uint32_t 
   Fa = Fa + c.ct * Vr;
   Ma = Ma + c.cr * wr;
   Mbw = Mbw - c.cr * wr;
+  if (!(R(1) + c.alpha_mean * dT > R(0))) d.clk->fault = 1;  // S:205
+}
 
+// The parts of voxel a that every bond of a shares.
+template <class R> struct AFrame {
+  Rot<R> Ra;
+  V3<R> ua, Va, wa;
+  int mat;
+};
+template <class R> __device__ __forceinline__ AFrame<R> a_frame(const Dev<R>& d, const VS<R>& a) {
+  AFrame<R> f;
+  const uint32_t meta = meta_of(a.p.w);
+  f.mat = meta & M_MAT;
+  const MatC<R>& M = d.mat[f.mat];
+  f.Ra = rotation(a.q.w, a.q.x, a.q.y, a.q.z);
+  f.ua = mk(a.p.x, a.p.y, a.p.z);
+  f.Va = M.inv_m * mk(a.mo.x, a.mo.y, a.mo.z);
+  f.wa = M.inv_I * mk(a.mo.w, a.an.x, a.an.y);
+  return f;
+}
+
+template <int AX, class R>
+__device__ __forceinline__ void bond_one(const Dev<R>& d, uint32_t ia, uint32_t ib,
+                                         const AFrame<R>& f, const typename VT<R>::R4& qa, R dT) {
+  using R4 = typename VT<R>::R4;
+  const VS<R> b = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, ib);
+  V3<R> Fa, Ma, Mbw;
+  bond_eval<AX>(d, f.Ra, qa, f.ua, f.Va, f.wa, f.mat, b, dT, Fa, Ma, Mbw);
   const size_t o = (size_t)AX * d.nloc + ia;
   d.recA[o] = R4{Fa.x, Fa.y, Fa.z, Ma.x};
   d.recB[o] = R4{Ma.y, Ma.z, Mbw.x, Mbw.y};
   d.recC[o] = Mbw.z;
-  if (!(R(1) + c.alpha_mean * dT > R(0))) d.clk->fault = 1;  // S:205
 }
 
 template <class R>
 __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 4 : 2) k_bonds(Dev<R> d, uint32_t beg, uint32_t end) {
-  using R4 = typename VT<R>::R4;
-  using R2 = typename VT<R>::R2;
   const uint32_t id = beg + blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= end) return;
-  const R4 pa = d.pos[id];
+  const typename VT<R>::R4 pa = d.pos[id];
   const uint32_t meta = meta_of(pa.w);
   const uint32_t want = meta & (nb_bit(1) | nb_bit(3) | nb_bit(5));
   if (!want) return;
-  const R4 qa = d.quat[id];
-  const R4 moa = d.mom[id];
-  const R2 ana = d.ang[id];
-  const int mat_a = meta & M_MAT;
-  const MatC<R>& Ma = d.mat[mat_a];
-  const Rot<R> Ra = rotation(qa.w, qa.x, qa.y, qa.z);
-  const V3<R> ua = mk(pa.x, pa.y, pa.z);
-  const V3<R> Va = Ma.inv_m * mk(moa.x, moa.y, moa.z);
-  const V3<R> wa = Ma.inv_I * mk(moa.w, ana.x, ana.y);
+  VS<R> a;
+  a.p = pa;
+  a.q = d.quat[id];
+  a.mo = d.mom[id];
+  a.an = d.ang[id];
+  const AFrame<R> f = a_frame(d, a);
   const R dT = (R)d.clk->dT;
-  if (want & nb_bit(1)) bond_one<0>(d, id, id + d.sx, Ra, qa, ua, Va, wa, mat_a, dT);
-  if (want & nb_bit(3)) bond_one<1>(d, id, id + d.nz, Ra, qa, ua, Va, wa, mat_a, dT);
-  if (want & nb_bit(5)) bond_one<2>(d, id, id + 1, Ra, qa, ua, Va, wa, mat_a, dT);
+  if (want & nb_bit(1)) bond_one<0>(d, id, id + d.sx, f, a.q, dT);
+  if (want & nb_bit(3)) bond_one<1>(d, id, id + d.nz, f, a.q, dT);
+  if (want & nb_bit(5)) bond_one<2>(d, id, id + 1, f, a.q, dT);
 }
 
 // ------------------------------------------------------------------ K4 integrate
+// Rotation increment below this squared angle uses the series of cos(a/2) and
+// sin(a/2)/a through a^6 (next term < 1e-17 relative at the cut).
+template <class R> struct IncCut;
+template <> struct IncCut<float> { static constexpr float a2 = 0.05f * 0.05f; };
+template <> struct IncCut<double> { static constexpr double a2 = 0.01 * 0.01; };
+
+// Stores of the new state are never re-read by the same kernel: evict-first.
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(float2* p, float2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double4* p, double4 v) {
+  double2* q = reinterpret_cast<double2*>(p);
+  __stcs(q, make_double2(v.x, v.y));
+  __stcs(q + 1, make_double2(v.z, v.w));
+}
+__device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
+
+// After the slot sums (Eq. 25-26): external force, gravity, ground
+// damping (R12), contacts, floor + friction (R14, R15),
+// integration (Eq. 27-30); writes the new state of `id` to the out arrays.
+template <class R, bool COLLIDE>
+__device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, const VS<R>& s, uint32_t meta,
+                                          V3<R> F, V3<R> M, typename VT<R>::R4* __restrict__ opos,
+                                          typename VT<R>::R4* __restrict__ oquat,
+                                          typename VT<R>::R4* __restrict__ omom,
+                                          typename VT<R>::R2* __restrict__ oang,
+                                          const uint32_t* __restrict__ ext_of_local) {
+  using R4 = typename VT<R>::R4;
+  using R2 = typename VT<R>::R2;
+  const MatC<R> mc = d.mat[meta & M_MAT];
+  const R4& p = s.p;
+  const R4& mo = s.mo;
+  const R2& an = s.an;
+  if (meta & M_EXT) {
+    const R4 fe = d.fext[id];
+    F = F + mk(fe.x, fe.y, fe.z);
+  }
+  F.z = F.z - mc.mg;
+  const V3<R> V = mc.inv_m * mk(mo.x, mo.y, mo.z);
+  const V3<R> w = mc.inv_I * mk(mo.w, an.x, an.y);
+  if (d.ground) {                                     // P:254, R12
+    F = F - mc.cgt * V;
+    M = M - mc.cgr * w;
+  }
+  if constexpr (COLLIDE) {
+    if (meta & M_SURF) {
+      const R4 c = d.cf[id];
+      F = F + mk(c.x, c.y, c.z);
+    }
+  }
+  bool latch = (meta & M_LATCH) != 0;
+  bool zero_lat = false;
+  if (d.floor_on) {                                   // P:260-274, R14, R15
+    const R dT = (R)d.clk->dT;
+    const uint32_t kz = id % d.nz;
+    // penetration r_v - (D_z - z_floor), r_v = (l/2)(1 + alpha dT)
+    const R base = (R)(d.zbase_d + d.l_d * (double)kz);
+    const R pen = d.half_l * mc.alpha * dT - p.z - base;
+    if (pen > R(0)) {
+      R Fn = mc.kf * pen - mc.cfl * V.z;
+      if (Fn < R(0)) Fn = R(0);
+      F.z = F.z + Fn;
+      const R Flx = F.x, Fly = F.y;
+      const R Fl = vx_sqrt(Flx * Flx + Fly * Fly);
+      const R Vl = vx_sqrt(V.x * V.x + V.y * V.y);
+      if (latch) {
+        if (Fl <= mc.mu_s * Fn) {                     // Eq. 36 holds
+          F.x = R(0); F.y = R(0); zero_lat = true;
+        } else {                                      // break away, Eq. 37
+          latch = false;
+          F.x = Flx - mc.mu_d * Fn * Flx / Fl;
+          F.y = Fly - mc.mu_d * Fn * Fly / Fl;
+        }
+      } else {
+        if (Vl <= mc.mu_d * Fn * mc.dt_m) {           // Eq. 38 halt
+          F.x = R(0); F.y = R(0); zero_lat = true; latch = true;
+        } else {
+          F.x = Flx - mc.mu_d * Fn * V.x / Vl;
+          F.y = Fly - mc.mu_d * Fn * V.y / Vl;
+        }
+      }
+    } else {
+      latch = false;
+    }
+  }
+  // Eq. 27-30
+  V3<R> P = mk(mo.x, mo.y, mo.z) + d.dt * F;
+  if (zero_lat) { P.x = R(0); P.y = R(0); }
+  const V3<R> u = mk(p.x, p.y, p.z) + mc.dt_m * P;
+  const V3<R> phi = mk(mo.w, an.x, an.y) + d.dt * M;
+  // q <- normalize(quat(th) (x) q), quat(th) = (cos(a/2), sin(a/2) th/a), a = |th|
+  const V3<R> th = mc.dt_I * phi;
+  const R a2 = dot(th, th);
+  R dw, ks;
+  if (a2 < IncCut<R>::a2) {   // per-step angles are tiny: Taylor series, no sincos
+    dw = R(1) - a2 * (R(1) / R(8) - a2 * (R(1) / R(384) - a2 * (R(1) / R(46080))));
+    ks = R(0.5) - a2 * (R(1) / R(48) - a2 * (R(1) / R(3840) - a2 * (R(1) / R(645120))));
+  } else {
+    const R a = vx_sqrt(a2);
+    R sh;
+    vx_sincos(R(0.5) * a, &sh, &dw);
+    ks = sh / a;
+  }
+  const R dx = ks * th.x, dy = ks * th.y, dz = ks * th.z;
+  const R4& q = s.q;
+  R qw = dw * q.w - dx * q.x - dy * q.y - dz * q.z;
+  R qx = dw * q.x + dx * q.w + dy * q.z - dz * q.y;
+  R qy = dw * q.y - dx * q.z + dy * q.w + dz * q.x;
+  R qz = dw * q.z + dx * q.y - dy * q.x + dz * q.w;
+  const R qi = R(1) / vx_sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+  qw = qw * qi; qx = qx * qi; qy = qy * qi; qz = qz * qi;
+  const uint32_t nmeta = latch ? (meta | M_LATCH) : (meta & ~M_LATCH);
+  st_stream(opos + id, R4{u.x, u.y, u.z, meta_as(R(0), nmeta)});
+  st_stream(oquat + id, R4{qx, qy, qz, qw});
+  st_stream(omom + id, R4{P.x, P.y, P.z, phi.x});
+  st_stream(oang + id, R2{phi.y, phi.z});
+  const bool ok = vx_finite(u.x) && vx_finite(u.y) && vx_finite(u.z) && vx_finite(qw) &&
+                  vx_finite(qx) && vx_finite(qy) && vx_finite(qz) && vx_finite(P.x) &&
+                  vx_finite(P.y) && vx_finite(P.z) && vx_finite(phi.x) && vx_finite(phi.y) &&
+                  vx_finite(phi.z);
+  if (!ok) {
+    const unsigned long long code =
+        ((unsigned long long)d.clk->step << 32) | (unsigned long long)ext_of_local[id];
+    atomicMin(&d.clk->err, code);
+  }
+  return COLLIDE ? vx_sqrt(dot(P, P)) * mc.inv_m : R(0);
+}
+
+// Block max of |V| -> motion budget.  All threads of the block call it.
+template <class R> __device__ __forceinline__ void budget_max(const Dev<R>& d, R v) {
+  __shared__ R sm[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sm[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? sm[lane] : R(0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0 && v > R(0)) {
+      using UB = typename VT<R>::UB;
+      atomicMax((UB*)&d.clk->vmax_bits, (UB)rbits(v));
+    }
+  }
+}
+
 template <class R, bool COLLIDE>
 __global__ void __launch_bounds__(256) k_integrate(Dev<R> d, uint32_t beg, uint32_t end,
                                                    const uint32_t* __restrict__ ext_of_local) {
   using R4 = typename VT<R>::R4;
-  using R2 = typename VT<R>::R2;
   const uint32_t id = beg + blockIdx.x * blockDim.x + threadIdx.x;
   R vmax = R(0);
   if (id < end) {
     const R4 p = d.pos[id];
     const uint32_t meta = meta_of(p.w);
     if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
-      const MatC<R> mc = d.mat[meta & M_MAT];
-      const R4 mo = d.mom[id];
-      const R2 an = d.ang[id];
+      VS<R> s;
+      s.p = p;
+      s.mo = d.mom[id];
+      s.an = d.ang[id];
       V3<R> F = mk(R(0), R(0), R(0)), M = F;
       const uint32_t strides[3] = {d.sx, d.nz, 1u};
       // Eq. 25-26 in slot order -x,+x,-y,+y,-z,+z: a -axis slot holds the
@@ -286,114 +466,155 @@ __global__ void __launch_bounds__(256) k_integrate(Dev<R> d, uint32_t beg, uint3
           M = M + mk(A.w, B.x, B.y);
         }
       }
-      if (meta & M_EXT) {
-        const R4 fe = d.fext[id];
-        F = F + mk(fe.x, fe.y, fe.z);
-      }
-      F.z = F.z - mc.mg;
-      const V3<R> V = mc.inv_m * mk(mo.x, mo.y, mo.z);
-      const V3<R> w = mc.inv_I * mk(mo.w, an.x, an.y);
-      if (d.ground) {                                     // P:254, R12
-        F = F - mc.cgt * V;
-        M = M - mc.cgr * w;
-      }
-      if constexpr (COLLIDE) {
-        if (meta & M_SURF) {
-          const R4 c = d.cf[id];
-          F = F + mk(c.x, c.y, c.z);
+      s.q = d.quat[id];
+      vmax = finish_voxel<R, COLLIDE>(d, id, s, meta, F, M, d.pos, d.quat, d.mom, d.ang,
+                                      ext_of_local);
+    }
+  }
+  if constexpr (COLLIDE) budget_max(d, vmax);
+}
+
+// ------------------------------------------------------------------ fused step (NEXT f1)
+// One pass per step: reads S_n (in), writes S_{n+1} (out), bond loads never
+// touch HBM.  A block owns rows [j0, j0+TY) of x-planes [i0, i1) over the full
+// z range (thread = k, nz <= blockDim.x) and sweeps x.  Per voxel it computes
+// its +x, +y, +z bonds exactly as K3 does (bond_eval); the -x slot is its own
+// previous-plane +x bond (shared memory), the -y slot its previous row's +y
+// bond (registers), the -z slot the +z bond of thread k-1 (shared memory).
+// Halo: the +y bond of row j0-1 per plane and the +x bond of plane i0-1 per
+// segment are recomputed.  The slot sums and finish_voxel are K4's, in K4's
+// order, so the update is the two-kernel update.
+template <class R> struct Rec6 {   // (F_a, M_b): what the "b" side of a bond needs
+  R f[6];
+};
+template <class R> struct FusedArgs {
+  typename VT<R>::R4* opos;
+  typename VT<R>::R4* oquat;
+  typename VT<R>::R4* omom;
+  typename VT<R>::R2* oang;
+  const uint32_t* ext_of_local;
+  int ty;           // rows per block
+  int sx;           // planes per segment
+  int p0, p1;       // local planes to update [p0, p1)
+  int ntiles_y;
+};
+
+template <class R, bool COLLIDE>
+__global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a) {
+  using R4 = typename VT<R>::R4;
+  using R2 = typename VT<R>::R2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nzb = blockDim.x;
+  // shared: xrec[ty][nzb] (Rec6), rowstate[nzb + 1] (VS), zrec[nzb] (Rec6)
+  Rec6<R>* xrec = reinterpret_cast<Rec6<R>*>(smem_raw);
+  VS<R>* rowst = reinterpret_cast<VS<R>*>(xrec + (size_t)a.ty * nzb);
+  Rec6<R>* zrec = reinterpret_cast<Rec6<R>*>(rowst + nzb + 1);
+
+  const int k = threadIdx.x;
+  const bool act = k < (int)d.nz;
+  const int tile = blockIdx.x % a.ntiles_y;
+  const int seg = blockIdx.x / a.ntiles_y;
+  const int j0 = tile * a.ty;
+  const int j1 = min(j0 + a.ty, (int)d.ny);
+  const int i0 = a.p0 + seg * a.sx;
+  const int i1 = min(i0 + a.sx, a.p1);
+  const uint32_t sx = d.sx, nz = d.nz;
+  const R dT = (R)d.clk->dT;
+  R vmax = R(0);
+  auto idx = [&](int i, int j) { return (uint32_t)i * sx + (uint32_t)j * nz + (uint32_t)k; };
+
+  // -x slots of plane i0: the +x bonds of plane i0 - 1 (halo, recomputed)
+  if (act)
+    for (int j = j0; j < j1; ++j) {
+      Rec6<R> r{};
+      if (i0 > 0) {
+        const uint32_t ia = idx(i0 - 1, j);
+        const VS<R> va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, ia);
+        if (meta_of(va.p.w) & nb_bit(1)) {
+          const VS<R> vb = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, ia + sx);
+          const AFrame<R> f = a_frame(d, va);
+          V3<R> Fa, Ma, Mb;
+          bond_eval<0>(d, f.Ra, va.q, f.ua, f.Va, f.wa, f.mat, vb, dT, Fa, Ma, Mb);
+          r = Rec6<R>{{Fa.x, Fa.y, Fa.z, Mb.x, Mb.y, Mb.z}};
         }
       }
-      bool latch = (meta & M_LATCH) != 0;
-      bool zero_lat = false;
-      if (d.floor_on) {                                   // P:260-274, R14, R15
-        const R dT = (R)d.clk->dT;
-        const uint32_t kz = id % d.nz;
-        // penetration r_v - (D_z - z_floor), r_v = (l/2)(1 + alpha dT)
-        const R base = (R)(d.zbase_d + d.l_d * (double)kz);
-        const R pen = d.half_l * mc.alpha * dT - p.z - base;
-        if (pen > R(0)) {
-          R Fn = mc.kf * pen - mc.cfl * V.z;
-          if (Fn < R(0)) Fn = R(0);
-          F.z = F.z + Fn;
-          const R Flx = F.x, Fly = F.y;
-          const R Fl = vx_sqrt(Flx * Flx + Fly * Fly);
-          const R Vl = vx_sqrt(V.x * V.x + V.y * V.y);
-          if (latch) {
-            if (Fl <= mc.mu_s * Fn) {                     // Eq. 36 holds
-              F.x = R(0); F.y = R(0); zero_lat = true;
-            } else {                                      // break away, Eq. 37
-              latch = false;
-              F.x = Flx - mc.mu_d * Fn * Flx / Fl;
-              F.y = Fly - mc.mu_d * Fn * Fly / Fl;
-            }
-          } else {
-            if (Vl <= mc.mu_d * Fn * mc.dt_m) {           // Eq. 38 halt
-              F.x = R(0); F.y = R(0); zero_lat = true; latch = true;
-            } else {
-              F.x = Flx - mc.mu_d * Fn * V.x / Vl;
-              F.y = Fly - mc.mu_d * Fn * V.y / Vl;
-            }
+      xrec[(size_t)(j - j0) * nzb + k] = r;
+    }
+
+  for (int i = i0; i < i1; ++i) {
+    VS<R> cur{};
+    Rec6<R> ry{};   // -y slot record of the current row: +y bond of the row below
+    if (act) {
+      cur = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0));
+      if (j0 > 0) {   // halo row j0 - 1: its +y bond only
+        const VS<R> vh = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0 - 1));
+        if (meta_of(vh.p.w) & nb_bit(3)) {
+          const AFrame<R> f = a_frame(d, vh);
+          V3<R> Fa, Ma, Mb;
+          bond_eval<1>(d, f.Ra, vh.q, f.ua, f.Va, f.wa, f.mat, cur, dT, Fa, Ma, Mb);
+          ry = Rec6<R>{{Fa.x, Fa.y, Fa.z, Mb.x, Mb.y, Mb.z}};
+        }
+      }
+    }
+    for (int j = j0; j < j1; ++j) {
+      const uint32_t meta = meta_of(cur.p.w);
+      VS<R> ny_{};   // next row: the +y neighbour and the next row's voxel
+      if (act && (j + 1 < j1 || (meta & nb_bit(3))))
+        ny_ = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j + 1));
+      VS<R> nx_{};
+      if (act && (meta & nb_bit(1))) nx_ = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j) + sx);
+      __syncthreads();                       // previous row done with rowst / zrec
+      if (act) rowst[k] = cur;
+      __syncthreads();
+      V3<R> FX{}, MX{}, BX{}, FY{}, MY{}, BY{}, FZ{}, MZ{}, BZ{};
+      if (act && (meta & M_FILLED)) {
+        const AFrame<R> f = a_frame(d, cur);
+        if (meta & nb_bit(1)) bond_eval<0>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nx_, dT, FX, MX, BX);
+        if (meta & nb_bit(3)) bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, ny_, dT, FY, MY, BY);
+        if (meta & nb_bit(5)) {
+          const VS<R> vz = rowst[k + 1];
+          bond_eval<2>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vz, dT, FZ, MZ, BZ);
+        }
+      }
+      if (act) zrec[k] = Rec6<R>{{FZ.x, FZ.y, FZ.z, BZ.x, BZ.y, BZ.z}};
+      __syncthreads();
+      if (act && (meta & M_FILLED)) {
+        const uint32_t id = idx(i, j);
+        Rec6<R>& xr = xrec[(size_t)(j - j0) * nzb + k];
+        if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
+          V3<R> F = mk(R(0), R(0), R(0)), M = F;
+          if (meta & nb_bit(0)) { F = F - mk(xr.f[0], xr.f[1], xr.f[2]); M = M + mk(xr.f[3], xr.f[4], xr.f[5]); }
+          if (meta & nb_bit(1)) { F = F + FX; M = M + MX; }
+          if (meta & nb_bit(2)) { F = F - mk(ry.f[0], ry.f[1], ry.f[2]); M = M + mk(ry.f[3], ry.f[4], ry.f[5]); }
+          if (meta & nb_bit(3)) { F = F + FY; M = M + MY; }
+          if (meta & nb_bit(4)) {
+            const Rec6<R>& zr = zrec[k - 1];
+            F = F - mk(zr.f[0], zr.f[1], zr.f[2]);
+            M = M + mk(zr.f[3], zr.f[4], zr.f[5]);
           }
-        } else {
-          latch = false;
+          if (meta & nb_bit(5)) { F = F + FZ; M = M + MZ; }
+          const R v = finish_voxel<R, COLLIDE>(d, id, cur, meta, F, M, a.opos, a.oquat, a.omom,
+                                               a.oang, a.ext_of_local);
+          vmax = fmax(vmax, v);
+        } else {   // fixed: copied through unchanged
+          a.opos[id] = cur.p;
+          a.oquat[id] = cur.q;
+          a.omom[id] = cur.mo;
+          a.oang[id] = cur.an;
         }
+        xr = Rec6<R>{{FX.x, FX.y, FX.z, BX.x, BX.y, BX.z}};
+      } else if (act) {
+        a.opos[idx(i, j)] = cur.p;     // empty cell: meta only
       }
-      // Eq. 27-30
-      V3<R> P = mk(mo.x, mo.y, mo.z) + d.dt * F;
-      if (zero_lat) { P.x = R(0); P.y = R(0); }
-      const V3<R> u = mk(p.x, p.y, p.z) + mc.dt_m * P;
-      const V3<R> phi = mk(mo.w, an.x, an.y) + d.dt * M;
-      const V3<R> th = mc.dt_I * phi;
-      const R a = vx_sqrt(dot(th, th));
-      R dw = R(1), dx = R(0), dy = R(0), dz = R(0);
-      if (a > R(0)) {
-        R sh, ch;
-        vx_sincos(R(0.5) * a, &sh, &ch);
-        const R sa = sh / a;
-        dw = ch; dx = sa * th.x; dy = sa * th.y; dz = sa * th.z;
-      }
-      const R4 q = d.quat[id];
-      R qw = dw * q.w - dx * q.x - dy * q.y - dz * q.z;
-      R qx = dw * q.x + dx * q.w + dy * q.z - dz * q.y;
-      R qy = dw * q.y - dx * q.z + dy * q.w + dz * q.x;
-      R qz = dw * q.z + dx * q.y - dy * q.x + dz * q.w;
-      const R qn = vx_sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
-      qw = qw / qn; qx = qx / qn; qy = qy / qn; qz = qz / qn;
-      const uint32_t nmeta = latch ? (meta | M_LATCH) : (meta & ~M_LATCH);
-      d.pos[id] = R4{u.x, u.y, u.z, meta_as(R(0), nmeta)};
-      d.quat[id] = R4{qx, qy, qz, qw};
-      d.mom[id] = R4{P.x, P.y, P.z, phi.x};
-      d.ang[id] = R2{phi.y, phi.z};
-      const bool ok = vx_finite(u.x) && vx_finite(u.y) && vx_finite(u.z) && vx_finite(qw) &&
-                      vx_finite(qx) && vx_finite(qy) && vx_finite(qz) && vx_finite(P.x) &&
-                      vx_finite(P.y) && vx_finite(P.z) && vx_finite(phi.x) &&
-                      vx_finite(phi.y) && vx_finite(phi.z);
-      if (!ok) {
-        const unsigned long long code =
-            ((unsigned long long)d.clk->step << 32) | (unsigned long long)ext_of_local[id];
-        atomicMin(&d.clk->err, code);
-      }
-      if constexpr (COLLIDE) vmax = vx_sqrt(dot(P, P)) * mc.inv_m;
+      ry = Rec6<R>{{FY.x, FY.y, FY.z, BY.x, BY.y, BY.z}};
+      cur = ny_;
     }
   }
-  if constexpr (COLLIDE) {   // block max of |V| -> motion budget
-    __shared__ R sm[8];
-    R v = vmax;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) sm[warp] = v;
-    __syncthreads();
-    if (warp == 0) {
-      v = lane < (int)(blockDim.x >> 5) ? sm[lane] : R(0);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (lane == 0 && v > R(0)) {
-        using UB = typename VT<R>::UB;
-        atomicMax((UB*)&d.clk->vmax_bits, (UB)rbits(v));
-      }
-    }
-  }
+  if constexpr (COLLIDE) budget_max(d, vmax);
+}
+
+template <class R> size_t fused_smem(int ty, int nzb) {
+  return sizeof(Rec6<R>) * ((size_t)ty * nzb + nzb) + sizeof(VS<R>) * (nzb + 1);
 }
 
 // ------------------------------------------------------------------ K5 broadphase

@@ -227,6 +227,17 @@ class Lattice:
         names = ("bonds", "integrate", "other", "all")
         return {k: (ms[i], cnt[i]) for i, k in enumerate(names)}
 
+    ENGINES = {"two_pass": 0, "fused": 1}
+
+    def set_engine(self, engine):
+        """'two_pass' (K3 + K4) or 'fused' (one kernel per step)."""
+        _check(N.load().vx_set_engine(self._h, self.ENGINES.get(engine, engine)))
+
+    @property
+    def engine(self):
+        e = int(N.load().vx_get_engine(self._h))
+        return {v: k for k, v in self.ENGINES.items()}.get(e, e)
+
     @property
     def launches_per_step(self):
         return int(N.load().vx_launches_per_step(self._h))
@@ -237,7 +248,7 @@ def create_lattice(*a, **kw) -> Lattice:
 
 
 def from_scene(scene, precision=None, device=0, rank=0, nranks=1, nccl_id=None,
-               init_state=True) -> Lattice:
+               init_state=True, engine=None) -> Lattice:
     """Convenience: a Lattice set up from a workloads.Scene (no arithmetic).
     ``init_state=False`` keeps the library's initial state (at rest on the
     lattice sites), which equals the scene's when it has no v0."""
@@ -245,6 +256,8 @@ def from_scene(scene, precision=None, device=0, rank=0, nranks=1, nccl_id=None,
                                  precision or scene.precision, device, rank, nranks, nccl_id)
     lat.set_materials(scene.materials)
     lat.set_environment(scene.env)
+    if engine is not None:
+        lat.set_engine(engine)
     if scene.fixed is not None or scene.fext is not None:
         lat.set_boundary(scene.fixed, scene.fext)
     for kind, org, size, force in scene.extra.get("regions", []):
