@@ -122,6 +122,8 @@ struct vx_lattice {
   long long N = 0, nbonds = 0, nsurf = 0;
   std::vector<long long> box_of_ext;      // global box id of each external voxel
   int max_cell = 0;
+  std::vector<uint8_t> pair_present;      // [256 * mat_a + mat_b] of every bond (a on the - side)
+  double alpha_lo = 0, alpha_hi = 0;      // extremes of (alpha_a + alpha_b)/2 over present pairs
   // boundary (external order)
   std::vector<uint8_t> fixed;
   std::vector<double> fext;
@@ -205,6 +207,7 @@ vx_status build_topology(vx_lattice* h) {
   h->nbonds = 0;
   h->nsurf = 0;
   h->surf_local.clear();
+  h->pair_present.assign(256 * 256, 0);
   const int di[6] = {-1, 1, 0, 0, 0, 0}, dj[6] = {0, 0, -1, 1, 0, 0}, dk[6] = {0, 0, 0, 0, -1, 1};
   for (int i = 0; i < nx; ++i)
     for (int j = 0; j < ny; ++j)
@@ -213,12 +216,17 @@ vx_status build_topology(vx_lattice* h) {
         if (!c) continue;
         uint32_t m = (uint32_t)(c - 1) | M_FILLED;
         int cnt = 0;
-        for (int s = 0; s < 6; ++s)
-          if (cell(i + di[s], j + dj[s], k + dk[s])) {
+        for (int s = 0; s < 6; ++s) {
+          const int cb = cell(i + di[s], j + dj[s], k + dk[s]);
+          if (cb) {
             m |= nb_bit(s);
             ++cnt;
-            if (s & 1) ++h->nbonds;
+            if (s & 1) {
+              ++h->nbonds;
+              h->pair_present[(size_t)(c - 1) * 256 + (cb - 1)] = 1;
+            }
           }
+        }
         if (cnt < 6) {
           m |= M_SURF;
           ++h->nsurf;
@@ -333,6 +341,8 @@ template <class R> vx_status upload_tables(vx_lattice* h) {
   std::vector<PairC<R>> pc((size_t)n * n);
   std::vector<MatD> md(n);
   for (int i = 0; i < n; ++i) md[i] = mat_d(h->mats[i], l);
+  h->alpha_lo = 0;
+  h->alpha_hi = 0;
   for (int i = 0; i < n; ++i) {
     const MatD& m = md[i];
     MatC<R>& c = mc[i];
@@ -360,11 +370,18 @@ template <class R> vx_status upload_tables(vx_lattice* h) {
       p.a1 = (R)a1; p.a2 = (R)a2; p.b1 = (R)b1; p.b2 = (R)b2; p.b3 = (R)b3;
       p.alpha_mean = (R)(0.5 * (md[i].cte + md[j].cte));
       const double mmin = std::min(md[i].m, md[j].m), Imin = std::min(md[i].I, md[j].I);
-      p.ct = (R)(2 * e.zeta_bond * std::sqrt(mmin * a1));   // Eq. 34, R10
-      p.cr = (R)(2 * e.zeta_bond * std::sqrt(Imin * a2));   // Eq. 35, R11
+      const double ct = 2 * e.zeta_bond * std::sqrt(mmin * a1);   // Eq. 34, R10
+      const double cr = 2 * e.zeta_bond * std::sqrt(Imin * a2);   // Eq. 35, R11
+      p.ct2 = (R)(0.5 * ct);
+      p.ct4 = (R)(0.25 * ct);
+      p.cr2 = (R)(0.5 * cr);
       p.inv_m_b = (R)(1.0 / md[j].m);
       p.inv_I_b = (R)(1.0 / md[j].I);
-      p.pad0 = p.pad1 = (R)0;
+      p.pad0 = (R)0;
+      if (h->pair_present[(size_t)i * 256 + j]) {   // Eq. 40 fault bounds
+        h->alpha_lo = std::min(h->alpha_lo, 0.5 * (md[i].cte + md[j].cte));
+        h->alpha_hi = std::max(h->alpha_hi, 0.5 * (md[i].cte + md[j].cte));
+      }
     }
   VX_TRY(h->mat.alloc(mc.size() * sizeof(MatC<R>)));
   VX_TRY(h->pair.alloc(pc.size() * sizeof(PairC<R>)));
@@ -499,6 +516,7 @@ template <class R> vx_status launch_fused(vx_lattice* h, const Slab& s, bool col
   a.ntiles_y = (h->ny + a.ty - 1) / a.ty;
   a.p0 = s.x0 - s.xl0;
   a.p1 = s.x1 - s.xl0;
+  a.nplanes = s.xl1 - s.xl0;
   const int planes = a.p1 - a.p0;
   const int target = 148 * 8;   // blocks: ~4 waves at 2 resident blocks per SM
   const int nseg = std::max(1, std::min(planes, (target + a.ntiles_y - 1) / a.ntiles_y));
@@ -580,7 +598,8 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
   const bool col = h->collide();
   if (ev) VX_CUDA(cudaEventRecord(ev[0], h->stream));
   ClockArgs ca{h->clk.as<Clock>(), h->dt, h->env.T_amp, h->env.T_freq, h->env.T_phase,
-               0.5 * h->env.horizon_voxels * h->l, col ? 1 : 0, h->prec};
+               0.5 * h->env.horizon_voxels * h->l, h->alpha_lo, h->alpha_hi, col ? 1 : 0,
+               h->prec};
   k_clock<<<1, 32, 0, h->stream>>>(ca);
   if (col) {
     const Dev<R> d = make_dev<R>(h, h->slabs[0]);

@@ -60,6 +60,7 @@ struct ClockArgs {
   Clock* clk;
   double dt, T_amp, T_freq, T_phase;
   double half_horizon;   // rebuild when budget >= horizon / 2
+  double alpha_lo, alpha_hi;   // extremes of alpha_mean over the lattice's bond pairs
   int collide, precision;
 };
 
@@ -69,7 +70,10 @@ __global__ void k_clock(ClockArgs a) {
   const long long n = c->next;
   const double t = (double)n * a.dt;
   const double PI = 3.14159265358979323846;
-  c->dT = a.T_amp * sin(2 * PI * a.T_freq * t + a.T_phase);
+  const double dT = a.T_amp * sin(2 * PI * a.T_freq * t + a.T_phase);
+  c->dT = dT;
+  // Eq. 40: a rest length l (1 + alpha_mean dT) <= 0 on any bond is a fault
+  if (!(1.0 + fmin(a.alpha_lo * dT, a.alpha_hi * dT) > 0.0)) c->fault = 1;
   c->step = n;
   c->next = n + 1;
   if (a.collide) {
@@ -215,21 +219,22 @@ __device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
   Ma = mul(Ra, to_world<AX>(ma));
   Mbw = mul(Ra, to_world<AX>(mbl));
 
-  // Eq. 33-35 in the world frame
+  // Eq. 33-35 in the world frame.  With the averages written out,
+  //   V_r = (V_b - V_avg) + (r/2) x w_avg = (V_b - V_a)/2 + (r x (w_a + w_b))/4
+  //   w_r = w_b - w_avg = (w_b - w_a)/2
+  // and c_t/2, c_t/4, c_r/2 come from the pair table (exact power-of-2 scalings).
   const V3<R> Vb = c.inv_m_b * mk(b.mo.x, b.mo.y, b.mo.z);
   const V3<R> wb = c.inv_I_b * mk(b.mo.w, b.an.x, b.an.y);
-  const V3<R> Vavg = R(0.5) * (Va + Vb);
-  const V3<R> wavg = R(0.5) * (wa + wb);
   V3<R> r = du;
   if constexpr (AX == 0) r.x += l;
   else if constexpr (AX == 1) r.y += l;
   else r.z += l;
-  const V3<R> Vr = (Vb - Vavg) + cross(R(0.5) * r, wavg);
-  const V3<R> wr = wb - wavg;
-  Fa = Fa + c.ct * Vr;
-  Ma = Ma + c.cr * wr;
-  Mbw = Mbw - c.cr * wr;
-  if (!(R(1) + c.alpha_mean * dT > R(0))) d.clk->fault = 1;
+  const V3<R> dV = Vb - Va;
+  const V3<R> rw = cross(r, wa + wb);
+  const V3<R> dw = wb - wa;
+  Fa = Fa + c.ct2 * dV + c.ct4 * rw;
+  Ma = Ma + c.cr2 * dw;
+  Mbw = Mbw - c.cr2 * dw;
 }
 
 // The parts of voxel a that every bond of a shares.
@@ -399,11 +404,10 @@ __device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, const VS
   st_stream(oquat + id, R4{qx, qy, qz, qw});
   st_stream(omom + id, R4{P.x, P.y, P.z, phi.x});
   st_stream(oang + id, R2{phi.y, phi.z});
-  const bool ok = vx_finite(u.x) && vx_finite(u.y) && vx_finite(u.z) && vx_finite(qw) &&
-                  vx_finite(qx) && vx_finite(qy) && vx_finite(qz) && vx_finite(P.x) &&
-                  vx_finite(P.y) && vx_finite(P.z) && vx_finite(phi.x) && vx_finite(phi.y) &&
-                  vx_finite(phi.z);
-  if (!ok) {
+  // any NaN/Inf among the 13 values: x * 0 is NaN exactly for non-finite x
+  const R z0 = (u.x + u.y + u.z + qw + qx + qy + qz) * R(0);
+  const R z1 = (P.x + P.y + P.z + phi.x + phi.y + phi.z) * R(0);
+  if (!(z0 + z1 == R(0))) {
     const unsigned long long code =
         ((unsigned long long)d.clk->step << 32) | (unsigned long long)ext_of_local[id];
     atomicMin(&d.clk->err, code);
@@ -497,6 +501,7 @@ template <class R> struct FusedArgs {
   int sx;           // planes per segment
   int p0, p1;       // local planes to update [p0, p1)
   int ntiles_y;
+  int nplanes;      // planes in the local box
 };
 
 template <class R, bool COLLIDE>
@@ -505,10 +510,9 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
   using R2 = typename VT<R>::R2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nzb = blockDim.x;
-  // shared: xrec[ty][nzb] (Rec6), rowstate[nzb + 1] (VS), zrec[nzb] (Rec6)
+  // shared: xrec[ty][nzb], zrec[2][nzb] (Rec6)
   Rec6<R>* xrec = reinterpret_cast<Rec6<R>*>(smem_raw);
-  VS<R>* rowst = reinterpret_cast<VS<R>*>(xrec + (size_t)a.ty * nzb);
-  Rec6<R>* zrec = reinterpret_cast<Rec6<R>*>(rowst + nzb + 1);
+  Rec6<R>* zrec = xrec + (size_t)a.ty * nzb;
 
   const int k = threadIdx.x;
   const bool act = k < (int)d.nz;
@@ -542,79 +546,79 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
     }
 
   for (int i = i0; i < i1; ++i) {
-    VS<R> cur{};
-    Rec6<R> ry{};   // -y slot record of the current row: +y bond of the row below
+    VS<R> va, vb;    // ping-pong: this row's voxel and the next row's
+    Rec6<R> ry{};    // -y slot record of the current row: +y bond of the row below
     if (act) {
-      cur = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0));
+      va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0));
       if (j0 > 0) {   // halo row j0 - 1: its +y bond only
         const VS<R> vh = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0 - 1));
         if (meta_of(vh.p.w) & nb_bit(3)) {
           const AFrame<R> f = a_frame(d, vh);
           V3<R> Fa, Ma, Mb;
-          bond_eval<1>(d, f.Ra, vh.q, f.ua, f.Va, f.wa, f.mat, cur, dT, Fa, Ma, Mb);
+          bond_eval<1>(d, f.Ra, vh.q, f.ua, f.Va, f.wa, f.mat, va, dT, Fa, Ma, Mb);
           ry = Rec6<R>{{Fa.x, Fa.y, Fa.z, Mb.x, Mb.y, Mb.z}};
         }
       }
     }
-    for (int j = j0; j < j1; ++j) {
-      const uint32_t meta = meta_of(cur.p.w);
-      VS<R> ny_{};   // next row: the +y neighbour and the next row's voxel
+    // One row: voxel (i, j, k) in `cur`; loads row j+1's voxel into `nxt`.  One
+    // block barrier: the -z slot (thread k-1's +z bond) goes through zrec[par].
+    auto row = [&](int j, const VS<R>& cur, VS<R>& nxt, int par) {
+      const uint32_t meta = act ? meta_of(cur.p.w) : 0u;
+      const uint32_t id = idx(i, j);
       if (act && (j + 1 < j1 || (meta & nb_bit(3))))
-        ny_ = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j + 1));
-      VS<R> nx_{};
-      if (act && (meta & nb_bit(1))) nx_ = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j) + sx);
-      __syncthreads();                       // previous row done with rowst / zrec
-      if (act) rowst[k] = cur;
-      __syncthreads();
+        nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
+      VS<R> vx, vz;
+      if (meta & nb_bit(1)) vx = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + sx);
+      if (meta & nb_bit(5)) vz = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + 1);   // L1: this row
       V3<R> FX{}, MX{}, BX{}, FY{}, MY{}, BY{}, FZ{}, MZ{}, BZ{};
-      if (act && (meta & M_FILLED)) {
+      if (meta & M_FILLED) {
         const AFrame<R> f = a_frame(d, cur);
-        if (meta & nb_bit(1)) bond_eval<0>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nx_, dT, FX, MX, BX);
-        if (meta & nb_bit(3)) bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, ny_, dT, FY, MY, BY);
-        if (meta & nb_bit(5)) {
-          const VS<R> vz = rowst[k + 1];
-          bond_eval<2>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vz, dT, FZ, MZ, BZ);
-        }
+        if (meta & nb_bit(5)) bond_eval<2>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vz, dT, FZ, MZ, BZ);
+        if (meta & nb_bit(1)) bond_eval<0>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vx, dT, FX, MX, BX);
+        if (meta & nb_bit(3)) bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nxt, dT, FY, MY, BY);
       }
-      if (act) zrec[k] = Rec6<R>{{FZ.x, FZ.y, FZ.z, BZ.x, BZ.y, BZ.z}};
-      __syncthreads();
-      if (act && (meta & M_FILLED)) {
-        const uint32_t id = idx(i, j);
-        Rec6<R>& xr = xrec[(size_t)(j - j0) * nzb + k];
-        if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
-          V3<R> F = mk(R(0), R(0), R(0)), M = F;
-          if (meta & nb_bit(0)) { F = F - mk(xr.f[0], xr.f[1], xr.f[2]); M = M + mk(xr.f[3], xr.f[4], xr.f[5]); }
-          if (meta & nb_bit(1)) { F = F + FX; M = M + MX; }
-          if (meta & nb_bit(2)) { F = F - mk(ry.f[0], ry.f[1], ry.f[2]); M = M + mk(ry.f[3], ry.f[4], ry.f[5]); }
-          if (meta & nb_bit(3)) { F = F + FY; M = M + MY; }
-          if (meta & nb_bit(4)) {
-            const Rec6<R>& zr = zrec[k - 1];
-            F = F - mk(zr.f[0], zr.f[1], zr.f[2]);
-            M = M + mk(zr.f[3], zr.f[4], zr.f[5]);
-          }
-          if (meta & nb_bit(5)) { F = F + FZ; M = M + MZ; }
-          const R v = finish_voxel<R, COLLIDE>(d, id, cur, meta, F, M, a.opos, a.oquat, a.omom,
-                                               a.oang, a.ext_of_local);
-          vmax = fmax(vmax, v);
-        } else {   // fixed: copied through unchanged
-          a.opos[id] = cur.p;
-          a.oquat[id] = cur.q;
-          a.omom[id] = cur.mo;
-          a.oang[id] = cur.an;
-        }
-        xr = Rec6<R>{{FX.x, FX.y, FX.z, BX.x, BX.y, BX.z}};
-      } else if (act) {
-        a.opos[idx(i, j)] = cur.p;     // empty cell: meta only
-      }
+      Rec6<R>* zr = zrec + (size_t)par * nzb;
+      if (act) zr[k] = Rec6<R>{{FZ.x, FZ.y, FZ.z, BZ.x, BZ.y, BZ.z}};
+      // K4's slot order -x, +x, -y, +y | -z, +z: the first four before the barrier
+      Rec6<R>& xr = xrec[(size_t)(j - j0) * nzb + k];
+      V3<R> F = mk(R(0), R(0), R(0)), M = F;
+      if (meta & nb_bit(0)) { F = F - mk(xr.f[0], xr.f[1], xr.f[2]); M = M + mk(xr.f[3], xr.f[4], xr.f[5]); }
+      if (meta & nb_bit(1)) { F = F + FX; M = M + MX; }
+      if (meta & nb_bit(2)) { F = F - mk(ry.f[0], ry.f[1], ry.f[2]); M = M + mk(ry.f[3], ry.f[4], ry.f[5]); }
+      if (meta & nb_bit(3)) { F = F + FY; M = M + MY; }
+      if (act && (meta & M_FILLED)) xr = Rec6<R>{{FX.x, FX.y, FX.z, BX.x, BX.y, BX.z}};
       ry = Rec6<R>{{FY.x, FY.y, FY.z, BY.x, BY.y, BY.z}};
-      cur = ny_;
+      __syncthreads();
+      if (!act) return;
+      if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
+        if (meta & nb_bit(4)) {
+          const Rec6<R>& z = zr[k - 1];
+          F = F - mk(z.f[0], z.f[1], z.f[2]);
+          M = M + mk(z.f[3], z.f[4], z.f[5]);
+        }
+        if (meta & nb_bit(5)) { F = F + FZ; M = M + MZ; }
+        const R v = finish_voxel<R, COLLIDE>(d, id, cur, meta, F, M, a.opos, a.oquat, a.omom,
+                                             a.oang, a.ext_of_local);
+        vmax = fmax(vmax, v);
+      } else if (meta & M_FILLED) {   // fixed: copied through unchanged
+        st_stream(a.opos + id, cur.p);
+        st_stream(a.oquat + id, cur.q);
+        st_stream(a.omom + id, cur.mo);
+        st_stream(a.oang + id, cur.an);
+      } else {
+        st_stream(a.opos + id, cur.p);   // empty cell: meta only
+      }
+    };
+    for (int j = j0; j < j1; ++j) {
+      row(j, va, vb, (j - j0) & 1);
+      va = vb;
     }
   }
   if constexpr (COLLIDE) budget_max(d, vmax);
 }
 
 template <class R> size_t fused_smem(int ty, int nzb) {
-  return sizeof(Rec6<R>) * ((size_t)ty * nzb + nzb) + sizeof(VS<R>) * (nzb + 1);
+  return sizeof(Rec6<R>) * ((size_t)ty * nzb + 2 * (size_t)nzb);
 }
 
 // ------------------------------------------------------------------ K5 broadphase
