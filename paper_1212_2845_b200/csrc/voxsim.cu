@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -157,6 +158,7 @@ struct vx_lattice {
 
   int engine = VX_ENGINE_TWO_PASS;
   bool fused_smem_set[2] = {false, false};
+  bool tma_ok = false;                    // TMA-staged fused variant (VX_FUSED_TMA=1; measured slower)
 
   bool fused() const { return engine == VX_ENGINE_FUSED; }
   bool fused_supported() const { return nz <= 256; }
@@ -512,27 +514,41 @@ template <class R> vx_status launch_fused(vx_lattice* h, const Slab& s, bool col
   a.omom = s.out(2).as<typename VT<R>::R4>();
   a.oang = s.out(3).as<typename VT<R>::R2>();
   a.ext_of_local = s.ext_of_local.as<uint32_t>();
-  a.ty = std::min(8, h->ny);
-  a.ntiles_y = (h->ny + a.ty - 1) / a.ty;
   a.p0 = s.x0 - s.xl0;
   a.p1 = s.x1 - s.xl0;
   a.nplanes = s.xl1 - s.xl0;
+  const int threads = ((h->nz + 31) / 32) * 32;
+  // TMA-staged rows need 16-byte aligned rows of every array (nz even); the
+  // rows per block are the most that keep two blocks per SM in shared memory.
+  const bool tma = h->tma_ok && (h->nz % 2 == 0);
+  int ty = std::min(8, h->ny);
+  if (tma)
+    while (ty > 1 && fused_tma_smem<R>(ty, threads) > 110 * 1024) --ty;
+  a.ty = ty;
+  a.ntiles_y = (h->ny + a.ty - 1) / a.ty;
   const int planes = a.p1 - a.p0;
   const int target = 148 * 8;   // blocks: ~4 waves at 2 resident blocks per SM
   const int nseg = std::max(1, std::min(planes, (target + a.ntiles_y - 1) / a.ntiles_y));
   a.sx = (planes + nseg - 1) / nseg;
   const int segs = (planes + a.sx - 1) / a.sx;
-  const int threads = ((h->nz + 31) / 32) * 32;
-  const size_t smem = fused_smem<R>(a.ty, threads);
   const int pi = sizeof(R) == 4 ? 0 : 1;
   if (!h->fused_smem_set[pi]) {
     VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    VX_CUDA(cudaFuncSetAttribute(k_step_fused_tma<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    VX_CUDA(cudaFuncSetAttribute(k_step_fused_tma<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     h->fused_smem_set[pi] = true;
   }
   const unsigned grid = (unsigned)(a.ntiles_y * segs);
-  if (col) k_step_fused<R, true><<<grid, threads, smem, h->stream>>>(d, a);
-  else k_step_fused<R, false><<<grid, threads, smem, h->stream>>>(d, a);
+  if (tma) {
+    const size_t smem = fused_tma_smem<R>(a.ty, threads);
+    if (col) k_step_fused_tma<R, true><<<grid, threads, smem, h->stream>>>(d, a);
+    else k_step_fused_tma<R, false><<<grid, threads, smem, h->stream>>>(d, a);
+  } else {
+    const size_t smem = fused_smem<R>(a.ty, threads);
+    if (col) k_step_fused<R, true><<<grid, threads, smem, h->stream>>>(d, a);
+    else k_step_fused<R, false><<<grid, threads, smem, h->stream>>>(d, a);
+  }
   return VX_OK;
 }
 
@@ -824,6 +840,7 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   h->prec = desc->precision;
   h->device = desc->device; h->rank = desc->rank; h->nranks = desc->nranks;
   h->emulated = emulated;
+  if (const char* e = std::getenv("VX_FUSED_TMA")) h->tma_ok = std::atoi(e) != 0;
   h->cells.assign(desc->cells, desc->cells + cells);
   h->plane = (uint32_t)((long long)h->ny * h->nz);
   h->nbox = (long long)h->nx * h->plane;

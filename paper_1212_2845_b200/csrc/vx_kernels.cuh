@@ -488,6 +488,16 @@ __global__ void __launch_bounds__(256) k_integrate(Dev<R> d, uint32_t beg, uint3
 // Halo: the +y bond of row j0-1 per plane and the +x bond of plane i0-1 per
 // segment are recomputed.  The slot sums and finish_voxel are K4's, in K4's
 // order, so the update is the two-kernel update.
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+template <class R> __device__ __forceinline__ void prefetch_vs(const Dev<R>& d, uint32_t i) {
+  prefetch_l1(d.pos + i);
+  prefetch_l1(d.quat + i);
+  prefetch_l1(d.mom + i);
+  prefetch_l1(d.ang + i);
+}
+
 template <class R> struct Rec6 {   // (F_a, M_b): what the "b" side of a bond needs
   R f[6];
 };
@@ -523,6 +533,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
   const int i0 = a.p0 + seg * a.sx;
   const int i1 = min(i0 + a.sx, a.p1);
   const uint32_t sx = d.sx, nz = d.nz;
+  const int ny = (int)d.ny;
   const R dT = (R)d.clk->dT;
   R vmax = R(0);
   auto idx = [&](int i, int j) { return (uint32_t)i * sx + (uint32_t)j * nz + (uint32_t)k; };
@@ -565,6 +576,11 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
     auto row = [&](int j, const VS<R>& cur, VS<R>& nxt, int par) {
       const uint32_t meta = act ? meta_of(cur.p.w) : 0u;
       const uint32_t id = idx(i, j);
+      // L1 prefetch of what row j+1 will load: (i, j+2) and (i+1, j+1)
+      if (act && j + 1 < j1) {
+        if (j + 2 < ny) prefetch_vs(d, id + 2 * nz);
+        if (i + 1 < a.nplanes) prefetch_vs(d, id + sx + nz);
+      }
       if (act && (j + 1 < j1 || (meta & nb_bit(3))))
         nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
       VS<R> vx, vz;
@@ -619,6 +635,220 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
 
 template <class R> size_t fused_smem(int ty, int nzb) {
   return sizeof(Rec6<R>) * ((size_t)ty * nzb + 2 * (size_t)nzb);
+}
+
+// ------------------------------------------------------------------ fused step, TMA-staged rows
+// Same sweep, same per-voxel arithmetic and order as k_step_fused; the voxel
+// rows it reads -- (i, j) for the voxel and its +z neighbour, (i, j+1) for +y,
+// (i+1, j) for +x -- are staged in shared memory by bulk copies
+// (cp.async.bulk, completion on one mbarrier per slot) issued by one thread
+// two rows ahead, so the compute warps never wait on HBM/L2 latency.
+// Needs nz even (16-byte aligned rows of every SoA array) and nz <= blockDim.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+template <class R> struct RowSlot {   // one staged voxel row (SoA, nzb entries)
+  typename VT<R>::R4* pos;
+  typename VT<R>::R4* quat;
+  typename VT<R>::R4* mom;
+  typename VT<R>::R2* ang;
+  __device__ VS<R> at(int k) const {
+    VS<R> v;
+    v.p = pos[k];
+    v.q = quat[k];
+    v.mo = mom[k];
+    v.an = ang[k];
+    return v;
+  }
+};
+template <class R> __device__ __forceinline__ RowSlot<R> row_slot(unsigned char* base, int nzb) {
+  using R4 = typename VT<R>::R4;
+  RowSlot<R> s;
+  s.pos = reinterpret_cast<R4*>(base);
+  s.quat = s.pos + nzb;
+  s.mom = s.quat + nzb;
+  s.ang = reinterpret_cast<typename VT<R>::R2*>(s.mom + nzb);
+  return s;
+}
+template <class R> __host__ __device__ constexpr size_t row_bytes(int nzb) {
+  return (size_t)nzb * (3 * sizeof(typename VT<R>::R4) + sizeof(typename VT<R>::R2));
+}
+
+constexpr int TMA_NX = 3;   // x-row slots: row j in use, rows j+1, j+2 in flight
+
+template <class R> size_t fused_tma_smem(int ty, int nzb) {
+  return TMA_NX * row_bytes<R>(nzb) + sizeof(Rec6<R>) * ((size_t)ty * nzb + 2 * (size_t)nzb) +
+         8 * TMA_NX + 16;
+}
+
+template <class R, bool COLLIDE>
+__global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R> a) {
+  using R4 = typename VT<R>::R4;
+  using R2 = typename VT<R>::R2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int nzb = blockDim.x;
+  const size_t rb = row_bytes<R>(nzb);
+  unsigned char* rows = smem_raw;                              // TMA_NX x-row slots
+  Rec6<R>* xrec = reinterpret_cast<Rec6<R>*>(rows + TMA_NX * rb);
+  Rec6<R>* zrec = xrec + (size_t)a.ty * nzb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(zrec + 2 * (size_t)nzb) + 15) & ~uintptr_t(15));
+
+  const int k = threadIdx.x;
+  const bool act = k < (int)d.nz;
+  const int tile = blockIdx.x % a.ntiles_y;
+  const int seg = blockIdx.x / a.ntiles_y;
+  const int j0 = tile * a.ty;
+  const int j1 = min(j0 + a.ty, (int)d.ny);
+  const int i0 = a.p0 + seg * a.sx;
+  const int i1 = min(i0 + a.sx, a.p1);
+  const uint32_t sx = d.sx, nz = d.nz;
+  const R dT = (R)d.clk->dT;
+  R vmax = R(0);
+  auto idx = [&](int i, int j) { return (uint32_t)i * sx + (uint32_t)j * nz + (uint32_t)k; };
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < TMA_NX; ++b) mbar_init(&bars[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // x-row stream: rows (i+1, j) for every row j of every plane i with i+1 in the
+  // box, issued by thread 0 TMA_NX - 1 rows ahead of use
+  long long x_iss = 0;
+  int xp = i0, xj = j0;
+  const uint32_t bytes = (uint32_t)(nz * (3 * sizeof(R4) + sizeof(R2)));
+  auto pump_x = [&](long long upto) {
+    while (x_iss < upto && xp < i1 && xp + 1 < a.nplanes) {
+      const int slot = (int)(x_iss % TMA_NX);
+      const RowSlot<R> s = row_slot<R>(rows + (size_t)slot * rb, nzb);
+      const uint32_t g = (uint32_t)(xp + 1) * sx + (uint32_t)xj * nz;
+      uint64_t* bar = &bars[slot];
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(s.pos, d.pos + g, nz * sizeof(R4), bar);
+      bulk_g2s(s.quat, d.quat + g, nz * sizeof(R4), bar);
+      bulk_g2s(s.mom, d.mom + g, nz * sizeof(R4), bar);
+      bulk_g2s(s.ang, d.ang + g, nz * sizeof(R2), bar);
+      ++x_iss;
+      if (++xj >= j1) { xj = j0; ++xp; }
+    }
+  };
+  if (threadIdx.x == 0) pump_x(TMA_NX - 1);
+
+  // -x slots of plane i0: the +x bonds of plane i0 - 1 (halo, recomputed)
+  if (act)
+    for (int j = j0; j < j1; ++j) {
+      Rec6<R> r{};
+      if (i0 > 0) {
+        const uint32_t ia = idx(i0 - 1, j);
+        const VS<R> va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, ia);
+        if (meta_of(va.p.w) & nb_bit(1)) {
+          const VS<R> vb = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, ia + sx);
+          const AFrame<R> f = a_frame(d, va);
+          V3<R> Fa, Ma, Mb;
+          bond_eval<0>(d, f.Ra, va.q, f.ua, f.Va, f.wa, f.mat, vb, dT, Fa, Ma, Mb);
+          r = Rec6<R>{{Fa.x, Fa.y, Fa.z, Mb.x, Mb.y, Mb.z}};
+        }
+      }
+      xrec[(size_t)(j - j0) * nzb + k] = r;
+    }
+
+  long long xe = 0;   // x-row element in use
+  for (int i = i0; i < i1; ++i) {
+    const bool hasx = i + 1 < a.nplanes;
+    VS<R> va, vb;
+    Rec6<R> ry{};
+    if (act) {
+      va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0));
+      if (j0 > 0) {   // halo row j0 - 1: its +y bond only
+        const VS<R> vh = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0 - 1));
+        if (meta_of(vh.p.w) & nb_bit(3)) {
+          const AFrame<R> f = a_frame(d, vh);
+          V3<R> Fa, Ma, Mb;
+          bond_eval<1>(d, f.Ra, vh.q, f.ua, f.Va, f.wa, f.mat, va, dT, Fa, Ma, Mb);
+          ry = Rec6<R>{{Fa.x, Fa.y, Fa.z, Mb.x, Mb.y, Mb.z}};
+        }
+      }
+    }
+    for (int j = j0; j < j1; ++j) {
+      const VS<R>& cur = va;
+      VS<R>& nxt = vb;
+      const uint32_t meta = act ? meta_of(cur.p.w) : 0u;
+      const uint32_t id = idx(i, j);
+      if (threadIdx.x == 0 && hasx) pump_x(xe + TMA_NX);
+      if (act && (j + 1 < j1 || (meta & nb_bit(3))))
+        nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
+      VS<R> vx, vz;
+      if (meta & nb_bit(5)) vz = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + 1);   // L1: this row
+      if (hasx) {
+        mbar_wait(&bars[xe % TMA_NX], (uint32_t)((xe / TMA_NX) & 1));
+        if (meta & nb_bit(1)) vx = row_slot<R>(rows + (size_t)(xe % TMA_NX) * rb, nzb).at(k);
+      }
+      V3<R> FX{}, MX{}, BX{}, FY{}, MY{}, BY{}, FZ{}, MZ{}, BZ{};
+      if (meta & M_FILLED) {
+        const AFrame<R> f = a_frame(d, cur);
+        if (meta & nb_bit(5)) bond_eval<2>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vz, dT, FZ, MZ, BZ);
+        if (meta & nb_bit(1)) bond_eval<0>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vx, dT, FX, MX, BX);
+        if (meta & nb_bit(3)) bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nxt, dT, FY, MY, BY);
+      }
+      Rec6<R>* zr = zrec + (size_t)((j - j0) & 1) * nzb;
+      if (act) zr[k] = Rec6<R>{{FZ.x, FZ.y, FZ.z, BZ.x, BZ.y, BZ.z}};
+      Rec6<R>& xr = xrec[(size_t)(j - j0) * nzb + k];
+      V3<R> F = mk(R(0), R(0), R(0)), M = F;
+      if (meta & nb_bit(0)) { F = F - mk(xr.f[0], xr.f[1], xr.f[2]); M = M + mk(xr.f[3], xr.f[4], xr.f[5]); }
+      if (meta & nb_bit(1)) { F = F + FX; M = M + MX; }
+      if (meta & nb_bit(2)) { F = F - mk(ry.f[0], ry.f[1], ry.f[2]); M = M + mk(ry.f[3], ry.f[4], ry.f[5]); }
+      if (meta & nb_bit(3)) { F = F + FY; M = M + MY; }
+      if (act && (meta & M_FILLED)) xr = Rec6<R>{{FX.x, FX.y, FX.z, BX.x, BX.y, BX.z}};
+      ry = Rec6<R>{{FY.x, FY.y, FY.z, BY.x, BY.y, BY.z}};
+      __syncthreads();   // z records visible; the x-row slot of row j may be refilled
+      if (hasx) ++xe;
+      if (act) {
+        if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
+          if (meta & nb_bit(4)) {
+            const Rec6<R>& z = zr[k - 1];
+            F = F - mk(z.f[0], z.f[1], z.f[2]);
+            M = M + mk(z.f[3], z.f[4], z.f[5]);
+          }
+          if (meta & nb_bit(5)) { F = F + FZ; M = M + MZ; }
+          const R v = finish_voxel<R, COLLIDE>(d, id, cur, meta, F, M, a.opos, a.oquat, a.omom,
+                                               a.oang, a.ext_of_local);
+          vmax = fmax(vmax, v);
+        } else if (meta & M_FILLED) {   // fixed: copied through unchanged
+          st_stream(a.opos + id, cur.p);
+          st_stream(a.oquat + id, cur.q);
+          st_stream(a.omom + id, cur.mo);
+          st_stream(a.oang + id, cur.an);
+        } else {
+          st_stream(a.opos + id, cur.p);   // empty cell: meta only
+        }
+      }
+      va = vb;
+    }
+  }
+  if constexpr (COLLIDE) budget_max(d, vmax);
 }
 
 // ------------------------------------------------------------------ K5 broadphase
