@@ -41,23 +41,30 @@ ALG_BYTES = {
     32: {"bonds": 56 + 108, "integrate": 108 + 56 + 56, "fused": 56 + 56},
     64: {"bonds": 112 + 216, "integrate": 216 + 112 + 112, "fused": 112 + 112},
 }
-# FP32 (FP64) lane-operations per voxel-step of the fused kernel, counted by ncu
-# (sass thread-instructions of the FADD/FMUL/FFMA/MUFU pipes, FFMA counted once;
-# profiles/); None until measured.
-ALU_OPS_PER_VOXEL = {32: None, 64: None}
+# Issue side of the fused kernel, counted by ncu on C5 fp32 (profiles/r03_fused.md):
+# warp-instructions per voxel-step (smsp__thread_inst_executed / 32) and FP32
+# lane-operations (FADD + FMUL + FFMA thread-instructions) per voxel-step.
+FUSED_COUNTS = {32: {"warp_inst": 922.8 / 32, "fp32_ops": 550.3}}
 
 
 def alu_roof(prec, ms, voxels, clocks):
-    ops = ALU_OPS_PER_VOXEL.get(prec)
-    if not ops:
+    """The fused single pass is bound by instruction issue, not by HBM: its
+    algorithmic intensity (855 FLOP / 112 B = 7.6 FLOP/B) sits below the FP32
+    ridge but its 29 warp-instructions per voxel need more issue cycles than
+    112 B need HBM time.  Peak = 4 warp-instructions / clock / SM x 148 SMs x
+    the median SM clock of the timed region."""
+    c = FUSED_COUNTS.get(prec)
+    if not c:
         return None
     mhz = (clocks or {}).get("sm_mhz") or 1965.0
-    lanes = 148 * 128 if prec == 32 else 148 * 64
-    peak = lanes * mhz * 1e6 / 1e12                    # Tops/s (1 op / lane / clock)
-    achieved = ops * voxels / (ms / 1e3) / 1e12
-    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-            "frac": achieved / peak, "ops_per_voxel": ops,
-            "peak_note": f"148 SMs x {lanes // 148} lanes x {mhz:.0f} MHz (median SM clock)"}
+    peak = 4 * 148 * mhz * 1e6 / 1e9                           # G warp-inst / s
+    achieved = c["warp_inst"] * voxels / (ms / 1e3) / 1e9
+    fp_peak = 128 * 148 * mhz * 1e6 / 1e12                     # T lane-ops / s
+    fp = c["fp32_ops"] * voxels / (ms / 1e3) / 1e12
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
+            "frac": achieved / peak, "warp_inst_per_voxel": c["warp_inst"],
+            "fp32": {"achieved": fp, "peak": fp_peak, "unit": "Tlane-op/s", "frac": fp / fp_peak},
+            "peak_note": f"4 issue/clk/SM x 148 SMs x {mhz:.0f} MHz; FP32 128 lanes/SM"}
 
 
 def _peaks():
@@ -275,8 +282,15 @@ def run_ours(args):
             "kernels": {k: {"ms_per_step": per_step_ms[k], "GBps": gbps[k]} for k in kinds},
             "step_GBps_alg": sum(alg[k] for k in kinds) * N / (ms_max / args.steps / 1e3) / 1e9}
     if fused:
-        # compute side of the single pass: FP32 lanes x clock
-        roof["alu"] = alu_roof(args.precision, per_step_ms[dom], vox_rank, clocks)
+        # the binding roof of the single pass is instruction issue (alu_roof)
+        alu = alu_roof(args.precision, per_step_ms[dom], vox_rank, clocks)
+        if alu:
+            hbm = {k: roof[k] for k in ("bound", "achieved", "peak", "peak_source", "unit", "frac",
+                                        "traffic", "alg_bytes_per_voxel")}
+            roof.update({k: alu[k] for k in ("bound", "achieved", "peak", "unit", "frac")})
+            roof["peak_source"] = alu["peak_note"]
+            roof["alu"] = alu
+            roof["hbm"] = hbm
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None

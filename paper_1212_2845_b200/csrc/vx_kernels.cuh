@@ -488,16 +488,6 @@ __global__ void __launch_bounds__(256) k_integrate(Dev<R> d, uint32_t beg, uint3
 // Halo: the +y bond of row j0-1 per plane and the +x bond of plane i0-1 per
 // segment are recomputed.  The slot sums and finish_voxel are K4's, in K4's
 // order, so the update is the two-kernel update.
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-template <class R> __device__ __forceinline__ void prefetch_vs(const Dev<R>& d, uint32_t i) {
-  prefetch_l1(d.pos + i);
-  prefetch_l1(d.quat + i);
-  prefetch_l1(d.mom + i);
-  prefetch_l1(d.ang + i);
-}
-
 template <class R> struct Rec6 {   // (F_a, M_b): what the "b" side of a bond needs
   R f[6];
 };
@@ -576,11 +566,6 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
     auto row = [&](int j, const VS<R>& cur, VS<R>& nxt, int par) {
       const uint32_t meta = act ? meta_of(cur.p.w) : 0u;
       const uint32_t id = idx(i, j);
-      // L1 prefetch of what row j+1 will load: (i, j+2) and (i+1, j+1)
-      if (act && j + 1 < j1) {
-        if (j + 2 < ny) prefetch_vs(d, id + 2 * nz);
-        if (i + 1 < a.nplanes) prefetch_vs(d, id + sx + nz);
-      }
       if (act && (j + 1 < j1 || (meta & nb_bit(3))))
         nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
       VS<R> vx, vz;
@@ -707,7 +692,7 @@ template <class R, bool COLLIDE>
 __global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R> a) {
   using R4 = typename VT<R>::R4;
   using R2 = typename VT<R>::R2;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nzb = blockDim.x;
   const size_t rb = row_bytes<R>(nzb);
   unsigned char* rows = smem_raw;                              // TMA_NX x-row slots
