@@ -159,6 +159,8 @@ struct vx_lattice {
   int engine = VX_ENGINE_TWO_PASS;
   bool fused_smem_set[2] = {false, false};
   bool tma_ok = false;                    // TMA-staged fused variant (VX_FUSED_TMA=1; measured slower)
+  int fused_ty = 8;                       // rows per fused block (VX_FUSED_TY overrides)
+  int fused_waves = 4;                    // block waves per fused launch (VX_FUSED_WAVES)
 
   bool fused() const { return engine == VX_ENGINE_FUSED; }
   bool fused_supported() const { return nz <= 256; }
@@ -171,9 +173,20 @@ struct vx_lattice {
     if (emulated) return (int)slabs.size();
     return nranks > 1 ? 3 : 1;
   }
+  // fused launches per step: one per slab, or interior + 2 boundary planes when
+  // slabs exchange ghost planes (NCCL ranks, emulated slabs)
+  int fused_launches() const {
+    if (!(emulated || nccl())) return (int)slabs.size();
+    int k = 0;
+    for (const auto& s : slabs) {
+      const int w = s.x1 - s.x0;
+      k += w >= 3 ? 3 : w;
+    }
+    return k;
+  }
   int launches_per_step() const {
-    int k = 1 + (int)slabs.size();                     // clock, integrate or fused
-    if (!fused()) k += bond_launches();                // bonds
+    int k = 1;                                         // clock
+    k += fused() ? fused_launches() : bond_launches() + (int)slabs.size();
     if (collide()) k += 2;
     return k;
   }
@@ -506,7 +519,9 @@ template <class R> void launch_integrate(vx_lattice* h, const Slab& s, const Dev
 
 // Fused single pass over a slab's owned planes: S_n (current copy) -> S_{n+1}
 // (other copy).  Block = one thread per z (nz <= 256) x TY rows x SX planes.
-template <class R> vx_status launch_fused(vx_lattice* h, const Slab& s, bool col) {
+template <class R>
+vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int x_end) {
+  if (x_end <= x_begin) return VX_OK;
   const Dev<R> d = make_dev<R>(h, s);
   FusedArgs<R> a;
   a.opos = s.out(0).as<typename VT<R>::R4>();
@@ -514,20 +529,20 @@ template <class R> vx_status launch_fused(vx_lattice* h, const Slab& s, bool col
   a.omom = s.out(2).as<typename VT<R>::R4>();
   a.oang = s.out(3).as<typename VT<R>::R2>();
   a.ext_of_local = s.ext_of_local.as<uint32_t>();
-  a.p0 = s.x0 - s.xl0;
-  a.p1 = s.x1 - s.xl0;
+  a.p0 = x_begin - s.xl0;
+  a.p1 = x_end - s.xl0;
   a.nplanes = s.xl1 - s.xl0;
   const int threads = ((h->nz + 31) / 32) * 32;
   // TMA-staged rows need 16-byte aligned rows of every array (nz even); the
   // rows per block are the most that keep two blocks per SM in shared memory.
   const bool tma = h->tma_ok && (h->nz % 2 == 0);
-  int ty = std::min(8, h->ny);
+  int ty = std::min(h->fused_ty, h->ny);
   if (tma)
     while (ty > 1 && fused_tma_smem<R>(ty, threads) > 110 * 1024) --ty;
   a.ty = ty;
   a.ntiles_y = (h->ny + a.ty - 1) / a.ty;
   const int planes = a.p1 - a.p0;
-  const int target = 148 * 8;   // blocks: ~4 waves at 2 resident blocks per SM
+  const int target = 148 * 2 * h->fused_waves;   // blocks: waves at 2 resident blocks per SM
   const int nseg = std::max(1, std::min(planes, (target + a.ntiles_y - 1) / a.ntiles_y));
   a.sx = (planes + nseg - 1) / nseg;
   const int segs = (planes + a.sx - 1) / a.sx;
@@ -633,15 +648,31 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
   if (h->emulated) VX_TRY(halo_local(h));
   if (ev) VX_CUDA(cudaEventRecord(ev[1], h->stream));
   if (h->fused()) {
-    if (h->nccl()) {   // ghost planes of S_n before the single pass
+    if (h->nccl()) {
+      // ghost planes of S_n on the comm stream, overlapped with the interior
+      // planes [x0+1, x1-1), which read no ghost plane; then the two boundary planes
+      const Slab& s = h->slabs[0];
       VX_CUDA(cudaEventRecord(h->ev_k4, h->stream));
       VX_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_k4, 0));
       VX_TRY(halo_nccl(h));
       VX_CUDA(cudaEventRecord(h->ev_halo, h->comm_stream));
+      if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
+      VX_TRY(launch_fused<R>(h, s, col, s.x0 + 1, s.x1 - 1));
       VX_CUDA(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+      VX_TRY(launch_fused<R>(h, s, col, s.x0, std::min(s.x0 + 1, s.x1)));
+      VX_TRY(launch_fused<R>(h, s, col, std::max(s.x1 - 1, s.x0 + 1), s.x1));
+    } else {
+      if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
+      for (const Slab& s : h->slabs) {
+        if (h->emulated) {   // the launch split of the NCCL ranks (ghosts already copied)
+          VX_TRY(launch_fused<R>(h, s, col, s.x0 + 1, s.x1 - 1));
+          VX_TRY(launch_fused<R>(h, s, col, s.x0, std::min(s.x0 + 1, s.x1)));
+          VX_TRY(launch_fused<R>(h, s, col, std::max(s.x1 - 1, s.x0 + 1), s.x1));
+        } else {
+          VX_TRY(launch_fused<R>(h, s, col, s.x0, s.x1));
+        }
+      }
     }
-    if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
-    for (const Slab& s : h->slabs) VX_TRY(launch_fused<R>(h, s, col));
     if (ev) VX_CUDA(cudaEventRecord(ev[3], h->stream));
     VX_CUDA(cudaGetLastError());
     h->flip();
@@ -688,7 +719,7 @@ template <class R> vx_status run_steps(vx_lattice* h, long long n) {
       VX_CUDA(cudaEventElapsedTime(&t, e[0], e[3]));
       h->t_ms[0] += a; h->t_ms[1] += b; h->t_ms[2] += c; h->t_ms[3] += t;
       h->t_cnt[0] += h->fused() ? 0 : h->bond_launches();
-      h->t_cnt[1] += (long long)h->slabs.size();
+      h->t_cnt[1] += h->fused() ? h->fused_launches() : (long long)h->slabs.size();
       h->t_cnt[2] += h->collide() ? 3 : 1;
       h->t_cnt[3] += h->launches_per_step();
     }
@@ -841,6 +872,8 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   h->device = desc->device; h->rank = desc->rank; h->nranks = desc->nranks;
   h->emulated = emulated;
   if (const char* e = std::getenv("VX_FUSED_TMA")) h->tma_ok = std::atoi(e) != 0;
+  if (const char* e = std::getenv("VX_FUSED_TY")) h->fused_ty = std::max(1, std::min(64, std::atoi(e)));
+  if (const char* e = std::getenv("VX_FUSED_WAVES")) h->fused_waves = std::max(1, std::min(64, std::atoi(e)));
   h->cells.assign(desc->cells, desc->cells + cells);
   h->plane = (uint32_t)((long long)h->ny * h->nz);
   h->nbox = (long long)h->nx * h->plane;

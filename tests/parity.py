@@ -38,10 +38,10 @@ def errors(gpu, orc, pos0, l):
     return dict(eD=eD, eP=eP, dq=dq)
 
 
-def run_pair(scene, steps, precision, chunks=1, threads=THREADS):
+def run_pair(scene, steps, precision, chunks=1, threads=THREADS, engine=None):
     """(gpu state, oracle state, initial positions, lattice, oracle)."""
     pos0 = scene.initial_state()[0]
-    lat = from_scene(scene, precision=precision)
+    lat = from_scene(scene, precision=precision, engine=engine)
     o = oracle_for(scene, threads)
     assert abs(lat.dt - o.dt) <= 1e-15 * o.dt
     per = steps // chunks

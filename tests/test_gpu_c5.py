@@ -41,9 +41,10 @@ def _samples(rng):
     return sorted(pts)
 
 
-def test_c5_full_size_sampled_one_step():
+@pytest.mark.parametrize("engine", ["fused", "two_pass"])
+def test_c5_full_size_sampled_one_step(engine):
     sc = W.block(precision=32)
-    lat = from_scene(sc, precision=32, init_state=False)
+    lat = from_scene(sc, precision=32, init_state=False, engine=engine)
     assert lat.num_voxels == NX * NY * NZ
     lat.step(3)        # bench warm-up
     lat.step(20)       # graph chunks

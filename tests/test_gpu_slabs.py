@@ -6,6 +6,7 @@ import pytest
 
 import workloads as W
 from paper_1212_2845_b200 import from_scene
+from paper_1212_2845_b200 import slab_planes as slab
 
 pytestmark = pytest.mark.gpu
 
@@ -28,17 +29,22 @@ def _scenes():
     return {"block": b, "walker": w, "cube": c, "cantilever": W.cantilever()}
 
 
+@pytest.mark.parametrize("engine", ["two_pass", "fused"])
 @pytest.mark.parametrize("prec", [32, 64])
 @pytest.mark.parametrize("name", ["block", "walker", "cube", "cantilever"])
-def test_slabs_bitwise_equal_single_domain(name, prec):
+def test_slabs_bitwise_equal_single_domain(name, prec, engine):
     sc = _scenes()[name]
-    ref = from_scene(sc, precision=prec)
+    ref = from_scene(sc, precision=prec, engine=engine)
     ref.step(150)
     r = _flat(ref.read_state())
     nx = sc.cells.shape[2]
     for P in sorted(p for p in {2, 3, 4, 5, 7, 8} if p <= nx):
-        lat = from_scene(sc, precision=prec, nranks=P)
-        assert lat.launches_per_step == 1 + 2 * P
+        lat = from_scene(sc, precision=prec, nranks=P, engine=engine)
+        if engine == "two_pass":
+            assert lat.launches_per_step == 1 + 2 * P
+        else:   # interior + two boundary planes per slab (fewer for thin slabs)
+            w = [b - a for a, b in (slab(nx, P, r) for r in range(P))]
+            assert lat.launches_per_step == 1 + sum(min(x, 3) for x in w)
         lat.step(150)
         assert np.array_equal(_flat(lat.read_state()), r), (name, prec, P)
         lat.destroy()
