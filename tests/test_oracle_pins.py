@@ -564,3 +564,40 @@ def test_divergence_names_voxel_and_step():
     o.set_state(pos, quat, P, phi, latch)
     with pytest.raises(FloatingPointError, match="voxel 1 at step 0"):
         o.step(5)
+
+
+# --------------------------------------------------------------- Table 2, Eq. 41
+def test_table2_modal_frequency_ratios():
+    """Thin-beam spectrum: f_n/f_1 within 7 % of the mass/spring
+    column (SPEC AC3) and within 1 % of the printed "analytical" column; f_1
+    bracketed by Eq. 41 with a span of 19 or 20 voxels (density not printed)."""
+    sc = W.cantilever(n=20, force=0.0, zeta_ground=0.0, E=1e6)
+    sc.env["zeta_bond"] = 0.01
+    o = OracleSim(sc.cells, L, sc.materials, sc.env)
+    o.set_threads(1)
+    o.set_boundary(sc.fixed, None)         # voxel (0,0,0) clamped, no static load
+    pos, quat, P, phi, latch = sc.initial_state()
+    P[-1, 2] = -1e-9                       # tip velocity -1 mm/s
+    o.set_state(pos, quat, P, phi, latch)
+    K, M = 10000, 40
+    z = np.empty(K)
+    for s in range(K):
+        o.step(M)
+        z[s] = o.read_state().pos[-1, 2]
+    f = np.fft.rfftfreq(K, M * o.dt)
+    S = np.abs(np.fft.rfft((z - z.mean()) * np.hanning(K)))
+    pk = []
+    for i in range(2, len(S) - 1):
+        if S[i] > S[i - 1] and S[i] >= S[i + 1] and S[i] > 1e-7 * S.max():
+            a, b, c = np.log(S[i - 1:i + 2])
+            pk.append((f[i] + 0.5 * (a - c) / (a - 2 * b + c) * (f[1] - f[0]), S[i]))
+    fr = np.array(sorted(x for x, _ in sorted(pk, key=lambda p: -p[1])[:6]))
+    rows = read_golden_table("table2.txt")
+    ms = np.array([float(r[2]) for r in rows])
+    an = np.array([float(r[1]) for r in rows])
+    ratio = fr / fr[0]
+    assert np.all(np.abs(ratio[1:] / (ms[1:] / ms[0]) - 1) <= 0.07), ratio
+    assert np.all(np.abs(ratio[1:] / (an[1:] / an[0]) - 1) <= 0.01), ratio
+    Kn1 = 3.5160
+    f1 = lambda span: Kn1 / (2 * math.pi) * math.sqrt(1e6 * L ** 4 / 12 / (1e-3 * span ** 4))
+    assert f1(20 * L) < fr[0] < f1(19 * L)
