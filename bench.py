@@ -218,9 +218,17 @@ def run_ours(args):
         nid = vd.bootstrap_nccl_id(dist, rank)
 
     sc = scene_for(args.config, args.precision)
-    lat = from_scene(sc, precision=args.precision, device=local, rank=rank, nranks=world,
-                     nccl_id=nid, init_state=sc.v0 is not None, engine=args.engine)
+    if args.engine == "auto":
+        args.engine = "fused" if 32 <= sc.cells.shape[0] <= 256 else "two_pass"
+    if args.batch > 1:   # K copies of the scene packed along x, one launch per step (f2)
+        from paper_1212_2845_b200.batch import pack
+        lat = pack([sc] * args.batch, precision=args.precision, engine=args.engine,
+                   device=local).lattice
+    else:
+        lat = from_scene(sc, precision=args.precision, device=local, rank=rank, nranks=world,
+                         nccl_id=nid, init_state=sc.v0 is not None, engine=args.engine)
     N = lat.num_voxels
+    st_init = lat.read_state() if args.batch > 1 and not args.no_e2e else None
     stream = torch.cuda.ExternalStream(lat.stream, device=torch.device("cuda", local))
 
     def barrier():
@@ -232,8 +240,12 @@ def run_ours(args):
     lat.step(max(args.warmup, 3))
     barrier()
 
-    # ---- timed region: K steps, state resident in HBM
-    lat.set_instrumentation(True)
+    # ---- timed region: K steps, state resident in HBM.  Per-kernel CUDA events
+    # are recorded inside the timed region (graphs off; launch overhead hidden by
+    # millisecond kernels) unless the lattice is small, where CUDA graphs carry the
+    # step and the kernel breakdown comes from a separate instrumented pass.
+    live = N >= 2_000_000 if args.timing == "auto" else args.timing == "live"
+    lat.set_instrumentation(live)
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
@@ -246,6 +258,9 @@ def run_ours(args):
     barrier()
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
+    if not live:
+        lat.set_instrumentation(True)
+        lat.step(min(args.steps, 50))
     kt = lat.kernel_times()
     lat.set_instrumentation(False)
     ms_max = vd.max_over_ranks([ms], dist if world > 1 else None, "cuda")[0]
@@ -253,7 +268,7 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (live CUDA-event durations)
     x0, x1 = lat.owned_planes()
-    vox_rank = N * (x1 - x0) / sc.cells.shape[2]   # dense boxes: voxels per rank
+    vox_rank = N if world == 1 else N * (x1 - x0) / sc.cells.shape[2]   # dense: per rank
     alg = ALG_BYTES[args.precision]
     fused = lat.engine == "fused"
     kinds = ("fused",) if fused else ("bonds", "integrate")
@@ -295,7 +310,8 @@ def run_ours(args):
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        st0 = sc.initial_state()
+        st0 = (sc.initial_state() if st_init is None else
+               (st_init.pos, st_init.quat, st_init.linmom, st_init.angmom, st_init.latch))
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa
         hin = [pin(a) for a in st0]
         from paper_1212_2845_b200 import State
@@ -335,8 +351,12 @@ def run_ours(args):
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
-            "config": {"workload": f"{sc.name} ({sc.cells.shape[2]}x{sc.cells.shape[1]}x"
+            "config": {"workload": (f"{args.batch} x " if args.batch > 1 else "") +
+                                   f"{sc.name} ({sc.cells.shape[2]}x{sc.cells.shape[1]}x"
                                    f"{sc.cells.shape[0]}, {N} voxels, {lat.num_bonds} bonds)",
+                       "engine": lat.engine,
+                       "timing": "per-kernel CUDA events in the timed region" if live else
+                                 "CUDA graphs; kernel breakdown from a separate instrumented pass",
                        "parallelism": f"x-slab{world}",
                        "l2": "no flush: working set (state + bond records) >> 126 MB L2"
                              if N > 1_000_000 else "small lattice, L2-resident"},
@@ -359,7 +379,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C5")
     ap.add_argument("--precision", type=int, default=32)
-    ap.add_argument("--engine", default="fused", choices=["fused", "two_pass"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "fused", "two_pass"],
+                    help="auto: the fused single pass when nz >= 32 (z lanes of a warp), else K3+K4")
+    ap.add_argument("--timing", default="auto", choices=["auto", "live", "graphs"],
+                    help="per-kernel events inside the timed region (live) or CUDA graphs")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="pack K copies of the config into one lattice (SURVEY 8f f2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -216,6 +216,17 @@ int32_t vx_launches_per_step(const vx_lattice* h);
  * nz <= 256 (INVALID_ARG otherwise).  In kernel timing (vx_kernel_times) the
  * fused kernel is reported in slot [1]. */
 typedef enum { VX_ENGINE_TWO_PASS = 0, VX_ENGINE_FUSED = 1 } vx_engine;
+
+/* Batched independent scenes (the design-automation use of
+ * "many, many physical evaluations"): the caller packs K scenes along x,
+ * scene s in planes [s*stride, s*stride + stride - 1) and an empty separator
+ * plane after each (no bonds cross it).  Declaring the stride makes self
+ * collision ignore pairs of different scenes, so every scene evolves exactly
+ * as it would alone (up to its x offset) while one launch steps all of them.
+ * stride 0 = one scene.  Errors: INVALID_ARG if a separator plane is not
+ * empty.  All scenes share the environment, the time step and the clock. */
+vx_status vx_set_batch(vx_lattice* h, int32_t stride);
+int32_t vx_num_scenes(const vx_lattice* h);
 vx_status vx_set_engine(vx_lattice* h, int32_t engine);
 int32_t vx_get_engine(const vx_lattice* h);
 

@@ -82,6 +82,8 @@ SIGNATURES = {
     "vx_kernel_times": (_I32, [_P, _DP, ctypes.POINTER(_I64)]),
     "vx_launches_per_step": (_I32, [_P]),
     "vx_set_engine": (_I32, [_P, _I32]),
+    "vx_set_batch": (_I32, [_P, _I32]),
+    "vx_num_scenes": (_I32, [_P]),
     "vx_get_engine": (_I32, [_P]),
     "vx_destroy": (None, [_P]),
     "vx_last_error": (ctypes.c_char_p, []),

@@ -161,6 +161,7 @@ struct vx_lattice {
   bool tma_ok = false;                    // TMA-staged fused variant (VX_FUSED_TMA=1; measured slower)
   int fused_ty = 8;                       // rows per fused block (VX_FUSED_TY overrides)
   int fused_waves = 4;                    // block waves per fused launch (VX_FUSED_WAVES)
+  int batch_stride = 0;                   // planes per batched scene (vx_set_batch)
 
   bool fused() const { return engine == VX_ENGINE_FUSED; }
   bool fused_supported() const { return nz <= 256; }
@@ -636,7 +637,8 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
     const Dev<R> d = make_dev<R>(h, h->slabs[0]);
     BroadArgs b{h->surf_d.as<int>(), (int)h->surf_local.size(), h->cellh.as<int4>(),
                 h->bcount.as<int>(), h->bstart.as<int>(), h->bitems.as<int>(),
-                h->rowptr.as<int>(), h->col.as<int>(), h->cap, h->H, h->clk.as<Clock>()};
+                h->rowptr.as<int>(), h->col.as<int>(), h->cap, h->H, h->clk.as<Clock>(),
+                h->batch_stride};
     const double hc = h->cutoff * 1.001;
     k_broadphase<R><<<1, 1024, 0, h->stream>>>(d, b, h->origin[0], h->origin[1], h->origin[2],
                                                (R)hc, (R)(h->cutoff * h->cutoff));
@@ -1366,6 +1368,28 @@ vx_status vx_kernel_times(vx_lattice* h, double out_ms[4], int64_t counts[4]) {
   return VX_OK;
 }
 int32_t vx_launches_per_step(const vx_lattice* h) { return h ? h->launches_per_step() : -1; }
+
+vx_status vx_set_batch(vx_lattice* h, int32_t stride) {
+  if (!h || stride < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
+  if (stride > 0) {
+    if (stride < 2) return fail(VX_ERR_INVALID_ARG, "a batched scene needs >= 1 plane + a separator");
+    // every stride-th plane (stride-1, 2 stride-1, ...) must be empty
+    for (int x = stride - 1; x < h->nx; x += stride)
+      for (long long c = 0; c < (long long)h->ny * h->nz; ++c) {
+        const long long j = c % h->ny, k = c / h->ny;
+        if (h->cells[(size_t)x + (size_t)h->nx * ((size_t)j + (size_t)h->ny * k)])
+          return fail(VX_ERR_INVALID_ARG, "separator plane x=" + std::to_string(x) + " is not empty");
+      }
+  }
+  h->batch_stride = stride;
+  h->clear_graphs();
+  VX_TRY(set_device(h));
+  return set_force_rebuild(h);
+}
+int32_t vx_num_scenes(const vx_lattice* h) {
+  if (!h) return -1;
+  return h->batch_stride ? (h->nx + h->batch_stride - 1) / h->batch_stride : 1;
+}
 
 vx_status vx_set_engine(vx_lattice* h, int32_t engine) {
   if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");

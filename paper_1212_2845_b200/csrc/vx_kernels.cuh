@@ -853,6 +853,7 @@ struct BroadArgs {
   long long cap;
   int H;              // power of two
   Clock* clk;
+  int batch_stride;   // planes per batched scene (0: one scene); no cross-scene pairs
 };
 
 __device__ __forceinline__ int cell_hash(int x, int y, int z, int H) {
@@ -947,6 +948,7 @@ __global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, doub
               int ib, jb, kb;
               surf_geom(d, idb, ib, jb, kb);
               if (abs(ia - ib) + abs(ja - jb) + abs(ka - kb) <= 3) continue;
+              if (b.batch_stride && ia / b.batch_stride != ib / b.batch_stride) continue;
               const typename VT<R>::R4 pb = d.pos[idb];
               const R rx = d.l * (R)(ia - ib) + (pa.x - pb.x);
               const R ry = d.l * (R)(ja - jb) + (pa.y - pb.y);

@@ -227,6 +227,14 @@ class Lattice:
         names = ("bonds", "integrate", "other", "all")
         return {k: (ms[i], cnt[i]) for i, k in enumerate(names)}
 
+    def set_batch(self, stride):
+        """Declare K scenes packed along x, `stride` planes each (incl. separator)."""
+        _check(N.load().vx_set_batch(self._h, int(stride)))
+
+    @property
+    def num_scenes(self):
+        return int(N.load().vx_num_scenes(self._h))
+
     ENGINES = {"two_pass": 0, "fused": 1}
 
     def set_engine(self, engine):

@@ -1,0 +1,67 @@
+"""Batched independent scenes: K scenes packed along x with
+separator planes, stepped by one launch per step, each evolving as it does
+alone -- including self collision, which vx_set_batch keeps inside a scene."""
+import numpy as np
+import pytest
+
+import workloads as W
+from paper_1212_2845_b200 import VoxError, from_scene
+from paper_1212_2845_b200.batch import pack
+
+pytestmark = pytest.mark.gpu
+
+
+def _cube_variants(K, n=6):
+    rng = np.random.default_rng(11)
+    out = []
+    for s in range(K):
+        sc = W.cube(contact_variant=True, n=n)
+        sc.cells = rng.integers(1, 3, size=sc.cells.shape).astype(np.uint8)   # a new design
+        out.append(sc)
+    return out
+
+
+@pytest.mark.parametrize("engine", ["fused", "two_pass"])
+@pytest.mark.parametrize("prec", [32, 64])
+def test_batch_equals_each_scene_alone(engine, prec):
+    scenes = _cube_variants(5)
+    b = pack(scenes, precision=prec, engine=engine)
+    assert b.lattice.num_scenes == 5
+    b.lattice.step(120)
+    st = b.lattice.read_state()
+    for s, sc in enumerate(scenes):
+        lat = from_scene(sc, precision=prec, engine=engine)
+        assert lat.dt == b.lattice.dt
+        lat.step(120)
+        ref = lat.read_state()
+        u_ref = ref.pos - sc.initial_state()[0]
+        u = b.displacement_of(s, st)
+        scale = np.abs(u_ref).max()
+        assert np.abs(u - u_ref).max() <= (1e-12 if prec == 64 else 1e-5) * scale, s
+        assert np.array_equal(st.latch[b.ext_of[s]], ref.latch)
+
+
+def test_batch_self_collision_stays_inside_each_scene():
+    # two-body collisions in every scene; bodies of neighbouring scenes are one
+    # plane apart, within the horizon, but must never be paired
+    scenes = [W.two_bodies(v=v) for v in (1.5, 2.0, 2.5)]
+    b = pack(scenes, precision=64)
+    b.lattice.step(300)
+    st = b.lattice.read_state()
+    pairs = b.lattice.contact_pairs()
+    scene_of = np.empty(sum(b.counts), int)
+    for s, ids in enumerate(b.ext_of):
+        scene_of[ids] = s
+    assert len(pairs) and np.all(scene_of[pairs[:, 0]] == scene_of[pairs[:, 1]])
+    for s, sc in enumerate(scenes):
+        lat = from_scene(sc, precision=64)
+        lat.step(300)
+        u_ref = lat.read_state().pos - sc.initial_state()[0]
+        assert np.abs(b.displacement_of(s, st) - u_ref).max() <= 1e-12 * np.abs(u_ref).max()
+
+
+def test_batch_rejects_filled_separator():
+    sc = W.cube(n=4)
+    lat = from_scene(sc, precision=32)
+    with pytest.raises(VoxError):
+        lat.set_batch(2)
