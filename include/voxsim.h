@@ -114,8 +114,12 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out);
 vx_status vx_set_materials(vx_lattice* h, const vx_material* palette, int32_t n);
 
 /* Environment and solver settings.  Errors: INVALID_ARG (damping ratio
- * outside [0,1], dt_safety outside (0,1], horizon <= 0, self_collision with
- * nranks > 1 -- not supported yet). */
+ * outside [0,1], dt_safety outside (0,1], horizon <= 0).  Self collision
+ * works with any slab count: each step every slab's surface-voxel state
+ * (32 B fp32 / 64 B fp64 per surface voxel) is broadcast to every rank, the
+ * motion budget takes the max |V| over all ranks (one allreduce), and each
+ * rank builds the shortlist rows of its own surface voxels;
+ * results are bitwise independent of the slab count. */
 vx_status vx_set_environment(vx_lattice* h, const vx_env* env);
 
 /* Per-voxel boundary conditions in external order, replacing previous ones:
@@ -181,14 +185,16 @@ int64_t vx_num_voxels(const vx_lattice* h);        /* N, global                 
 int64_t vx_num_bonds(const vx_lattice* h);         /* face-adjacent pairs, global   */
 int64_t vx_num_surface(const vx_lattice* h);       /* surface voxels, global */
 int64_t vx_steps_done(const vx_lattice* h);        /* step counter n                 */
-int64_t vx_num_contact_pairs(const vx_lattice* h); /* current shortlist size (pairs a<b) */
+int64_t vx_num_contact_pairs(const vx_lattice* h); /* current shortlist size (pairs a<b);
+                                                      collective over NCCL ranks */
 int64_t vx_num_rebuilds(const vx_lattice* h);      /* broadphase rebuilds so far     */
 int32_t vx_owned_planes(const vx_lattice* h, int32_t* x_begin, int32_t* x_end); /* this rank's x-slab */
 
 /* Copy the current collision shortlist as external-id pairs (a < b),
  * ascending, into pairs[2*cap]; returns the total number of pairs (which may
  * exceed cap), 0 when self collision is off, -1 on error.  The list holds
- * every surface pair within the horizon cutoff at the last rebuild. */
+ * every surface pair within the horizon cutoff at the last rebuild; over NCCL
+ * ranks, the pairs with at least one voxel in this rank's slab. */
 int64_t vx_contact_pairs(vx_lattice* h, int64_t* pairs, int64_t cap);
 
 /* The CUDA stream every kernel of this lattice is launched on (cudaStream_t).

@@ -139,9 +139,10 @@ struct vx_lattice {
   cudaStream_t stream = nullptr, comm_stream = nullptr;
   cudaEvent_t ev_k4 = nullptr, ev_halo = nullptr;
   DevBuf mat, pair, clk, box_of_ext_d, pair_w2, mat_w2;
-  // self collision (single slab only)
-  std::vector<int> surf_local;
-  DevBuf surf_d, cellh, bcount, bstart, bitems, rowptr, col;
+  // self collision: global surface table (kernels K5 / k_contact)
+  std::vector<unsigned> surf_g;           // global box id of every surface voxel, ascending
+  std::vector<int> seg;                   // nranks + 1: surface segment of each rank's slab
+  DevBuf surf_d, ss, cellh, bcount, bstart, bitems, rowptr, col;
   int H = 0;
   long long cap = 0;
   double cutoff = 0;
@@ -170,6 +171,14 @@ struct vx_lattice {
   }
   bool nccl() const { return nranks > 1 && !emulated; }
   bool collide() const { return env_set && env.self_collision && nsurf > 0; }
+  // surface rows this handle builds: its rank's segment over NCCL, else all
+  int rows_begin() const { return nccl() ? seg[rank] : 0; }
+  int rows_end() const { return nccl() ? seg[rank + 1] : seg[nranks]; }
+  // surface segment of slab q of this handle
+  int slab_seg(size_t q, int end) const {
+    const int r = emulated ? (int)q : rank;
+    return seg[r + end];
+  }
   int bond_launches() const {
     if (emulated) return (int)slabs.size();
     return nranks > 1 ? 3 : 1;
@@ -185,10 +194,12 @@ struct vx_lattice {
     }
     return k;
   }
+  // clock + (surface pack and contact per slab + broadphase when colliding)
+  int other_launches() const { return 1 + (collide() ? 1 + 2 * (int)slabs.size() : 0); }
   int launches_per_step() const {
     int k = 1;                                         // clock
     k += fused() ? fused_launches() : bond_launches() + (int)slabs.size();
-    if (collide()) k += 2;
+    if (collide()) k += other_launches() - 1;
     return k;
   }
   void clear_graphs() {
@@ -222,7 +233,7 @@ vx_status build_topology(vx_lattice* h) {
   for (auto& s : h->slabs) s.meta_static.assign(s.nloc, 0u);
   h->nbonds = 0;
   h->nsurf = 0;
-  h->surf_local.clear();
+  h->surf_g.clear();
   h->pair_present.assign(256 * 256, 0);
   const int di[6] = {-1, 1, 0, 0, 0, 0}, dj[6] = {0, 0, -1, 1, 0, 0}, dk[6] = {0, 0, 0, 0, -1, 1};
   for (int i = 0; i < nx; ++i)
@@ -246,15 +257,22 @@ vx_status build_topology(vx_lattice* h) {
         if (cnt < 6) {
           m |= M_SURF;
           ++h->nsurf;
+          h->surf_g.push_back((unsigned)(((long long)i * ny + j) * nz + k));
         }
         for (auto& s : h->slabs) {
           if (i < s.xl0 || i >= s.xl1) continue;
           const uint32_t li = (uint32_t)(((long long)(i - s.xl0) * ny + j) * nz + k);
           s.meta_static[li] = m;
-          if ((m & M_SURF) && h->slabs.size() == 1 && i >= s.x0 && i < s.x1)
-            h->surf_local.push_back((int)li);
         }
       }
+  // surface segment of every rank's slab (box order is x-slowest)
+  h->seg.assign((size_t)h->nranks + 1, 0);
+  for (int r = 0; r < h->nranks; ++r) {
+    int a, b;
+    slab_planes(nx, h->nranks, r, &a, &b);
+    h->seg[r] = (int)(std::lower_bound(h->surf_g.begin(), h->surf_g.end(), (unsigned)a * h->plane) - h->surf_g.begin());
+    h->seg[r + 1] = (int)(std::lower_bound(h->surf_g.begin(), h->surf_g.end(), (unsigned)b * h->plane) - h->surf_g.begin());
+  }
   return VX_OK;
 }
 
@@ -463,23 +481,27 @@ void update_dt(vx_lattice* h) {
 }
 
 vx_status setup_collision(vx_lattice* h) {
-  Slab& sl = h->slabs[0];
-  const int S = (int)h->surf_local.size();
+  const int S = (int)h->surf_g.size();
+  const size_t r = rsize(h->prec);
   VX_TRY(h->surf_d.alloc((size_t)std::max(S, 1) * 4));
-  if (S) VX_CUDA(cudaMemcpy(h->surf_d.p, h->surf_local.data(), (size_t)S * 4, cudaMemcpyHostToDevice));
+  if (S) VX_CUDA(cudaMemcpy(h->surf_d.p, h->surf_g.data(), (size_t)S * 4, cudaMemcpyHostToDevice));
+  VX_TRY(h->ss.alloc((size_t)std::max(S, 1) * 2 * 4 * r));
   int H = 1024;
   while (H < 2 * S) H <<= 1;
   h->H = H;
-  h->cap = std::max<long long>(1 << 16, 128LL * S);
+  const int rows = h->rows_end() - h->rows_begin();
+  h->cap = std::max<long long>(1 << 16, 128LL * rows);
   VX_TRY(h->cellh.alloc((size_t)std::max(S, 1) * sizeof(int4)));
   VX_TRY(h->bcount.alloc((size_t)H * 4));
   VX_TRY(h->bstart.alloc((size_t)(H + 1) * 4));
   VX_TRY(h->bitems.alloc((size_t)std::max(S, 1) * 4));
   VX_TRY(h->rowptr.alloc((size_t)(S + 1) * 4));
   VX_TRY(h->col.alloc((size_t)h->cap * 4));
-  VX_TRY(sl.cf.alloc((size_t)sl.nloc * 4 * rsize(h->prec)));
   VX_CUDA(cudaMemset(h->rowptr.p, 0, (size_t)(S + 1) * 4));
-  VX_CUDA(cudaMemset(sl.cf.p, 0, sl.cf.bytes));
+  for (Slab& sl : h->slabs) {
+    VX_TRY(sl.cf.alloc((size_t)sl.nloc * 4 * r));
+    VX_CUDA(cudaMemset(sl.cf.p, 0, sl.cf.bytes));
+  }
   // cutoff = 2 r_max + horizon, r_max = (l/2)(1 + max|alpha| |T_amp|)
   double amax = 0;
   for (auto& m : h->mats) amax = std::max(amax, std::fabs(m.cte));
@@ -632,20 +654,47 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
   ClockArgs ca{h->clk.as<Clock>(), h->dt, h->env.T_amp, h->env.T_freq, h->env.T_phase,
                0.5 * h->env.horizon_voxels * h->l, h->alpha_lo, h->alpha_hi, col ? 1 : 0,
                h->prec};
+  if (col && h->nccl()) {
+    // motion budget over the whole lattice: max |V| of every rank
+    unsigned long long* vb = &h->clk.as<Clock>()->vmax_bits;
+    VX_NCCL(ncclAllReduce(vb, vb, 1, ncclUint64, ncclMax, h->comm, h->stream));
+  }
   k_clock<<<1, 32, 0, h->stream>>>(ca);
   if (col) {
-    const Dev<R> d = make_dev<R>(h, h->slabs[0]);
-    BroadArgs b{h->surf_d.as<int>(), (int)h->surf_local.size(), h->cellh.as<int4>(),
+    using R4 = typename VT<R>::R4;
+    R4* ss = h->ss.as<R4>();
+    const unsigned* gb = h->surf_d.as<unsigned>();
+    for (size_t q = 0; q < h->slabs.size(); ++q) {
+      const int s0 = h->slab_seg(q, 0), s1 = h->slab_seg(q, 1);
+      if (s1 > s0)
+        k_surf_pack<R><<<grid_of(s1 - s0), 256, 0, h->stream>>>(make_dev<R>(h, h->slabs[q]), gb, s0, s1, ss);
+    }
+    if (h->nccl()) {   // every rank's segment of the surface table to every rank
+      VX_NCCL(ncclGroupStart());
+      for (int r = 0; r < h->nranks; ++r) {
+        const size_t cnt = (size_t)(h->seg[r + 1] - h->seg[r]) * 2 * sizeof(R4);
+        if (!cnt) continue;
+        char* p = reinterpret_cast<char*>(ss + 2 * (size_t)h->seg[r]);
+        VX_NCCL(ncclBroadcast(p, p, cnt, ncclInt8, r, h->comm, h->stream));
+      }
+      VX_NCCL(ncclGroupEnd());
+    }
+    const int S = (int)h->surf_g.size();
+    BroadArgs b{gb, S, h->rows_begin(), h->rows_end(), h->cellh.as<int4>(),
                 h->bcount.as<int>(), h->bstart.as<int>(), h->bitems.as<int>(),
                 h->rowptr.as<int>(), h->col.as<int>(), h->cap, h->H, h->clk.as<Clock>(),
                 h->batch_stride};
     const double hc = h->cutoff * 1.001;
-    k_broadphase<R><<<1, 1024, 0, h->stream>>>(d, b, h->origin[0], h->origin[1], h->origin[2],
-                                               (R)hc, (R)(h->cutoff * h->cutoff));
-    const int S = (int)h->surf_local.size();
-    if (S)
-      k_contact<R><<<grid_of(S), 256, 0, h->stream>>>(d, h->surf_d.as<int>(), S, h->rowptr.as<int>(),
-                                                      h->col.as<int>(), (R)h->env.zeta_col);
+    k_broadphase<R><<<1, 1024, 0, h->stream>>>(make_dev<R>(h, h->slabs[0]), b, ss, h->origin[0],
+                                               h->origin[1], h->origin[2], (R)hc,
+                                               (R)(h->cutoff * h->cutoff));
+    for (size_t q = 0; q < h->slabs.size(); ++q) {
+      const int s0 = h->slab_seg(q, 0), s1 = h->slab_seg(q, 1);
+      if (s1 > s0)
+        k_contact<R><<<grid_of(s1 - s0), 256, 0, h->stream>>>(make_dev<R>(h, h->slabs[q]), gb, ss, s0, s1,
+                                                               h->rowptr.as<int>(), h->col.as<int>(),
+                                                               (R)h->env.zeta_col);
+    }
   }
   if (h->emulated) VX_TRY(halo_local(h));
   if (ev) VX_CUDA(cudaEventRecord(ev[1], h->stream));
@@ -722,7 +771,7 @@ template <class R> vx_status run_steps(vx_lattice* h, long long n) {
       h->t_ms[0] += a; h->t_ms[1] += b; h->t_ms[2] += c; h->t_ms[3] += t;
       h->t_cnt[0] += h->fused() ? 0 : h->bond_launches();
       h->t_cnt[1] += h->fused() ? h->fused_launches() : (long long)h->slabs.size();
-      h->t_cnt[2] += h->collide() ? 3 : 1;
+      h->t_cnt[2] += h->other_launches();
       h->t_cnt[3] += h->launches_per_step();
     }
     return VX_OK;
@@ -995,8 +1044,6 @@ vx_status vx_set_environment(vx_lattice* h, const vx_env* e) {
   if (!(e->dt_safety > 0 && e->dt_safety <= 1)) return fail(VX_ERR_INVALID_ARG, "dt_safety must be in (0,1]");
   if (e->self_collision && !(e->horizon_voxels > 0))
     return fail(VX_ERR_INVALID_ARG, "horizon_voxels must be > 0");
-  if (e->self_collision && h->nranks > 1)
-    return fail(VX_ERR_INVALID_ARG, "self collision with nranks > 1 is not supported yet");
   const double v[] = {e->gravity, e->floor_z, e->T_ref, e->T_amp, e->T_freq, e->T_phase};
   for (double x : v)
     if (!std::isfinite(x)) return fail(VX_ERR_INVALID_ARG, "non-finite environment value");
@@ -1303,9 +1350,20 @@ int64_t vx_steps_done(const vx_lattice* h) { return h ? h->steps_done : -1; }
 
 int64_t vx_num_contact_pairs(const vx_lattice* h) {
   if (!h || !h->clk.p) return -1;
+  if (cudaSetDevice(h->device) != cudaSuccess) return -1;
   Clock c;
   if (cudaMemcpy(&c, h->clk.p, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  return c.npairs;
+  long long half = c.npairs;   // half-edges of the rows this handle built
+  if (h->nccl()) {             // collective: every rank's rows
+    DevBuf t;
+    if (t.alloc(8) != VX_OK) return -1;
+    if (cudaMemcpy(t.p, &half, 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+        ncclAllReduce(t.p, t.p, 1, ncclInt64, ncclSum, h->comm, h->stream) != ncclSuccess ||
+        cudaMemcpyAsync(&half, t.p, 8, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+        cudaStreamSynchronize(h->stream) != cudaSuccess)
+      return -1;
+  }
+  return half / 2;
 }
 int64_t vx_num_rebuilds(const vx_lattice* h) {
   if (!h || !h->clk.p) return -1;
@@ -1325,27 +1383,27 @@ int64_t vx_contact_pairs(vx_lattice* h, int64_t* pairs, int64_t cap) {
   if (!h) return -1;
   if (!h->collide() || h->tables_dirty || !h->rowptr.p) return 0;
   if (cudaSetDevice(h->device) != cudaSuccess) return -1;
-  const Slab& sl = h->slabs[0];
-  const int S = (int)h->surf_local.size();
+  const int S = (int)h->surf_g.size();
   std::vector<int> rp(S + 1);
   if (cudaMemcpy(rp.data(), h->rowptr.p, (size_t)(S + 1) * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   const long long tot = std::min<long long>(rp[S], h->cap);
   std::vector<int> col((size_t)std::max<long long>(tot, 1));
   if (tot && cudaMemcpy(col.data(), h->col.p, (size_t)tot * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  std::vector<long long> eol(sl.nloc, -1);
+  // external id of every surface index
+  std::vector<long long> ext(S, -1);
   for (long long e = 0; e < h->N; ++e) {
-    const long long li = h->box_of_ext[e] - sl.box_base;
-    if (li >= 0 && li < (long long)sl.nloc) eol[li] = e;
+    const unsigned g = (unsigned)h->box_of_ext[e];
+    auto it = std::lower_bound(h->surf_g.begin(), h->surf_g.end(), g);
+    if (it != h->surf_g.end() && *it == g) ext[it - h->surf_g.begin()] = e;
   }
   std::vector<std::pair<long long, long long>> out;
-  for (int s = 0; s < S; ++s) {
-    const long long a = eol[h->surf_local[s]];
+  for (int s = h->rows_begin(); s < h->rows_end(); ++s)
     for (int q = rp[s]; q < std::min<long long>(rp[s + 1], tot); ++q) {
-      const long long b = eol[col[q]];
-      if (a < b) out.emplace_back(a, b);
+      const long long a = ext[s], b = ext[col[q]];
+      out.emplace_back(std::min(a, b), std::max(a, b));
     }
-  }
   std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
   for (long long i = 0; i < (long long)out.size() && i < cap; ++i) {
     pairs[2 * i] = out[i].first;
     pairs[2 * i + 1] = out[i].second;

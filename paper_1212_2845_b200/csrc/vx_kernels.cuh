@@ -5,6 +5,7 @@
 //   k_bonds      K3: per-bond loads (Eq. 13-24, 33-35, 39-40)
 //   k_integrate  K4: fixed-order gather (Eq. 25-26), gravity, ground damping,
 //                contacts, floor + friction, integration (Eq. 27-30)
+//   k_surf_pack  surface table: each slab's surface-voxel state S_n
 //   k_broadphase K5: hashed-grid surface-voxel pair list
 //   k_contact    self-collision penalty loads on the shortlist
 // plus state scatter/gather for the C ABI.  Readings: DESIGN.md §3.
@@ -837,23 +838,42 @@ __global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R
 }
 
 // ------------------------------------------------------------------ K5 broadphase
-// One CTA (1024 threads), gated by clk->rebuild.  Surface voxels are hashed
-// by cell floor(D / h), h >= cutoff; every pair with |D_a - D_b| < cutoff and
-// lattice Manhattan distance > 3 goes into a both-direction CSR whose
-// rows are sorted by partner id (deterministic).
+// Surface table.  Every surface voxel of the whole lattice (all slabs) has a
+// global surface index s, ascending in global box id gbox[s] (x-slowest), so
+// each slab's surface voxels are one contiguous segment.  Each step the slabs
+// pack their segment's state S_n into ss (ss[2s] = pos, ss[2s+1] = mom) and,
+// over NCCL, broadcast it to every rank; the broadphase and the contact loads
+// then read only ss, so a slab sees partners owned by any other slab (SURVEY
+// §8f f3) and the arithmetic is the same for every slab count.
+template <class R>
+__global__ void __launch_bounds__(256) k_surf_pack(Dev<R> d, const unsigned* gbox, int s0, int s1,
+                                                  typename VT<R>::R4* ss) {
+  const int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= s1) return;
+  const unsigned li = gbox[s] - (unsigned)d.xl0 * d.sx;
+  ss[2 * s] = d.pos[li];
+  ss[2 * s + 1] = d.mom[li];
+}
+
+// One CTA (1024 threads), gated by clk->rebuild.  All S surface voxels are
+// hashed by cell floor(D / h), h >= cutoff; for the rows [r0, r1) (this
+// rank's segment, or every row in one process) each partner with
+// |D_a - D_b| < cutoff and lattice Manhattan distance > 3 goes into a
+// CSR of global surface indices, each row sorted ascending (deterministic).
 struct BroadArgs {
-  const int* surf;    // S local ids, ascending
-  int S;
-  int4* cellh;        // per surface voxel: cell x,y,z and hash
-  int* bcount;        // H
-  int* bstart;        // H + 1
-  int* bitems;        // S
-  int* rowptr;        // S + 1
-  int* col;           // cap
+  const unsigned* gbox;   // S global box ids, ascending
+  int S;                  // surface voxels of the whole lattice
+  int r0, r1;             // rows built here
+  int4* cellh;            // per surface voxel: cell x,y,z and hash
+  int* bcount;            // H
+  int* bstart;            // H + 1
+  int* bitems;            // S
+  int* rowptr;            // S + 1 (rows outside [r0, r1) are empty)
+  int* col;               // cap
   long long cap;
-  int H;              // power of two
+  int H;                  // power of two
   Clock* clk;
-  int batch_stride;   // planes per batched scene (0: one scene); no cross-scene pairs
+  int batch_stride;       // planes per batched scene (0: one scene); no cross-scene pairs
 };
 
 __device__ __forceinline__ int cell_hash(int x, int y, int z, int H) {
@@ -887,25 +907,27 @@ __device__ void cta_exscan(int* a, int n) {
   __syncthreads();
 }
 
+// global box id -> lattice indices (box order: x slowest, z fastest)
 template <class R>
-__device__ __forceinline__ void surf_geom(const Dev<R>& d, int id, int& i, int& j, int& k) {
-  k = id % (int)d.nz;
-  j = (id / (int)d.nz) % (int)d.ny;
-  i = id / (int)(d.nz * d.ny) + d.xl0;
+__device__ __forceinline__ void box_ijk(const Dev<R>& d, unsigned g, int& i, int& j, int& k) {
+  i = (int)(g / d.sx);
+  const unsigned r = g - (unsigned)i * d.sx;
+  j = (int)(r / d.nz);
+  k = (int)(r - (unsigned)j * d.nz);
 }
 
 template <class R>
-__global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, double ox,
-                                                     double oy, double oz, R h, R cutoff2) {
+__global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, const typename VT<R>::R4* ss,
+                                                     double ox, double oy, double oz, R h, R cutoff2) {
+  using R4 = typename VT<R>::R4;
   if (!d.clk->rebuild) return;
   const int T = blockDim.x, t = threadIdx.x;
   for (int x = t; x < b.H; x += T) b.bcount[x] = 0;
   __syncthreads();
   for (int s = t; s < b.S; s += T) {
-    const int id = b.surf[s];
     int i, j, k;
-    surf_geom(d, id, i, j, k);
-    const typename VT<R>::R4 p = d.pos[id];
+    box_ijk(d, b.gbox[s], i, j, k);
+    const R4 p = ss[2 * s];
     const R Dx = (R)(ox + d.l_d * ((double)i + 0.5)) + p.x;
     const R Dy = (R)(oy + d.l_d * ((double)j + 0.5)) + p.y;
     const R Dz = (R)(oz + d.l_d * ((double)k + 0.5)) + p.z;
@@ -928,11 +950,14 @@ __global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, doub
   // two passes: count, then fill (pass 1 writes rowptr, pass 2 col)
   for (int pass = 0; pass < 2; ++pass) {
     for (int s = t; s < b.S; s += T) {
+      if (s < b.r0 || s >= b.r1) {
+        if (!pass) b.rowptr[s] = 0;
+        continue;
+      }
       const int4 cs = b.cellh[s];
-      const int ida = b.surf[s];
       int ia, ja, ka;
-      surf_geom(d, ida, ia, ja, ka);
-      const typename VT<R>::R4 pa = d.pos[ida];
+      box_ijk(d, b.gbox[s], ia, ja, ka);
+      const R4 pa = ss[2 * s];
       int cnt = 0;
       const int base = pass ? b.rowptr[s] : 0;
       for (int dz = -1; dz <= 1; ++dz)
@@ -944,25 +969,24 @@ __global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, doub
               const int u = b.bitems[q];
               const int4 cu = b.cellh[u];
               if (u == s || cu.x != cx || cu.y != cy || cu.z != cz) continue;
-              const int idb = b.surf[u];
               int ib, jb, kb;
-              surf_geom(d, idb, ib, jb, kb);
+              box_ijk(d, b.gbox[u], ib, jb, kb);
               if (abs(ia - ib) + abs(ja - jb) + abs(ka - kb) <= 3) continue;
               if (b.batch_stride && ia / b.batch_stride != ib / b.batch_stride) continue;
-              const typename VT<R>::R4 pb = d.pos[idb];
+              const R4 pb = ss[2 * u];
               const R rx = d.l * (R)(ia - ib) + (pa.x - pb.x);
               const R ry = d.l * (R)(ja - jb) + (pa.y - pb.y);
               const R rz = d.l * (R)(ka - kb) + (pa.z - pb.z);
               if (rx * rx + ry * ry + rz * rz >= cutoff2) continue;
               if (pass) {
-                if (base + cnt < b.cap) b.col[base + cnt] = idb;
+                if (base + cnt < b.cap) b.col[base + cnt] = u;
               }
               ++cnt;
             }
           }
       if (!pass) {
         b.rowptr[s] = cnt;
-      } else if (base + cnt <= b.cap) {   // sort the row by partner id
+      } else if (base + cnt <= b.cap) {   // sort the row by partner index
         for (int x = base + 1; x < base + cnt; ++x) {
           const int v = b.col[x];
           int y = x - 1;
@@ -977,7 +1001,7 @@ __global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, doub
       if (t == 0) {
         const long long tot = b.rowptr[b.S];
         if (tot > b.cap) d.clk->overflow = 1;
-        d.clk->npairs = tot / 2;
+        d.clk->npairs = tot;          // half-edges of the rows built here
         d.clk->rebuilds += 1;
       }
       __syncthreads();
@@ -987,29 +1011,30 @@ __global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, doub
 
 // ------------------------------------------------------------------ contact
 // Penalty law of reading R16: F_on_a = max(0, k_c q - c_c v_n) n,
-// q = r_a + r_b - |D_a - D_b|; partners summed in ascending id.
+// q = r_a + r_b - |D_a - D_b|; partners summed in ascending surface index
+// (= ascending box id).  Rows [r0, r1) are one slab's segment; the load goes
+// to that slab's cf at the voxel's local id.
 template <class R>
-__global__ void __launch_bounds__(256) k_contact(Dev<R> d, const int* surf, int S,
-                                                 const int* rowptr, const int* col,
-                                                 R zeta_col) {
+__global__ void __launch_bounds__(256) k_contact(Dev<R> d, const unsigned* gbox,
+                                                 const typename VT<R>::R4* ss, int r0, int r1,
+                                                 const int* rowptr, const int* col, R zeta_col) {
   using R4 = typename VT<R>::R4;
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= S) return;
-  const int ida = surf[s];
+  const int s = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= r1) return;
   int ia, ja, ka;
-  surf_geom(d, ida, ia, ja, ka);
-  const R4 pa = d.pos[ida];
+  box_ijk(d, gbox[s], ia, ja, ka);
+  const R4 pa = ss[2 * s];
   const int mat_a = meta_of(pa.w) & M_MAT;
   const MatC<R>& ma = d.mat[mat_a];
-  const R4 moa = d.mom[ida];
+  const R4 moa = ss[2 * s + 1];
   const R dT = (R)d.clk->dT;
   const R ra = d.half_l * (R(1) + ma.alpha * dT);
   V3<R> F = mk(R(0), R(0), R(0));
   for (int q = rowptr[s]; q < rowptr[s + 1]; ++q) {
-    const int idb = col[q];
+    const int u = col[q];
     int ib, jb, kb;
-    surf_geom(d, idb, ib, jb, kb);
-    const R4 pb = d.pos[idb];
+    box_ijk(d, gbox[u], ib, jb, kb);
+    const R4 pb = ss[2 * u];
     const int mat_b = meta_of(pb.w) & M_MAT;
     const MatC<R>& mb = d.mat[mat_b];
     const R rb = d.half_l * (R(1) + mb.alpha * dT);
@@ -1020,8 +1045,8 @@ __global__ void __launch_bounds__(256) k_contact(Dev<R> d, const int* surf, int 
     if (!(pen > R(0))) continue;
     V3<R> n;
     if (dist > R(0)) n = (R(1) / dist) * dd;
-    else n = mk(R(0), R(0), ida < idb ? R(1) : R(-1));
-    const R4 mob = d.mom[idb];
+    else n = mk(R(0), R(0), s < u ? R(1) : R(-1));
+    const R4 mob = ss[2 * u + 1];
     const V3<R> Va = ma.inv_m * mk(moa.x, moa.y, moa.z);
     const V3<R> Vb = mb.inv_m * mk(mob.x, mob.y, mob.z);
     const R vn = dot(Va - Vb, n);
@@ -1031,7 +1056,7 @@ __global__ void __launch_bounds__(256) k_contact(Dev<R> d, const int* surf, int 
     if (f < R(0)) f = R(0);
     F = F + f * n;
   }
-  d.cf[ida] = R4{F.x, F.y, F.z, R(0)};
+  d.cf[gbox[s] - (unsigned)d.xl0 * d.sx] = R4{F.x, F.y, F.z, R(0)};
 }
 
 // ------------------------------------------------------------------ state I/O

@@ -1,6 +1,8 @@
 """The N>1 path's host logic on CPU with world_size-2 (and 3) gloo process
 groups: NCCL-id bootstrap, slab partition, the ghost-plane protocol (with gloo
-send/recv standing in for NCCL) and the max-over-ranks timing reduction."""
+send/recv standing in for NCCL), the self-collision surface-table protocol
+(per-rank segment broadcast + motion-budget max) and the max-over-ranks
+timing reduction."""
 import os
 import socket
 
@@ -58,7 +60,32 @@ def _worker(rank, world, port, q):
     if "R" in bufs:
         local[-1] = bufs["R"].numpy()
     out["ghosts_ok"] = bool(np.array_equal(local, glob[xl0:xl1]))
-    # 4. max over ranks of per-rank times
+    # 4. self-collision surface table, as libvoxsim runs it over
+    #    NCCL: surface voxels in global box order; rank r owns the contiguous
+    #    segment of its slab, packs it, and broadcasts it to every rank; the
+    #    motion budget takes the max |V| over ranks (one allreduce)
+    cells = rng.random((nx, ny, nz)) < 0.6
+    pad = np.pad(cells, 1)
+    nb = sum(np.roll(pad, s, a)[1:-1, 1:-1, 1:-1] for a in range(3) for s in (-1, 1))
+    surf = np.flatnonzero((cells & (nb < 6)).ravel())          # global box ids, ascending
+    state = rng.normal(size=(nx * ny * nz, 2))                  # (pos, mom) stand-ins
+    plane = ny * nz
+    seg = [int(np.searchsorted(surf, vd.ghost_planes(nx, world, r)[0] * plane)) for r in range(world)]
+    seg.append(len(surf))
+    table = torch.zeros(len(surf), 2, dtype=torch.float64)
+    mine = surf[seg[rank]:seg[rank + 1]]
+    assert np.all((mine // plane >= x0) & (mine // plane < x1))
+    table[seg[rank]:seg[rank + 1]] = torch.from_numpy(state[mine])
+    for r in range(world):
+        if seg[r + 1] > seg[r]:
+            part = table[seg[r]:seg[r + 1]].clone()
+            dist.broadcast(part, src=r)
+            table[seg[r]:seg[r + 1]] = part
+    out["table_ok"] = bool(np.array_equal(table.numpy(), state[surf]))
+    vmax = torch.tensor([float(np.abs(state[x0 * plane:x1 * plane, 1]).max())], dtype=torch.float64)
+    dist.all_reduce(vmax, op=dist.ReduceOp.MAX)
+    out["vmax_ok"] = float(vmax) == float(np.abs(state[:, 1]).max())
+    # 5. max over ranks of per-rank times
     out["max"] = vd.max_over_ranks([1.0 + rank, 10.0 - rank], dist)
     dist.destroy_process_group()
     q.put((rank, out))
@@ -83,4 +110,5 @@ def test_multirank_host_logic_gloo(world):
     assert max(sizes) - min(sizes) <= 1
     for r in range(world):
         assert res[r]["ids_equal"] and res[r]["ghosts_ok"]
+        assert res[r]["table_ok"] and res[r]["vmax_ok"]
         assert res[r]["max"] == [float(world), 10.0]
