@@ -52,7 +52,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
            "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
-           "-Xlinker", "-rpath," + os.path.join(nd, "lib"), "-o", tmp, *SOURCES]
+           "-Xlinker", "-rpath," + os.path.join(nd, "lib"), "-o", tmp, *SOURCES,
+           *os.environ.get("VX_NVCC_EXTRA", "").split()]   # experiments only
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -134,6 +134,92 @@ template <class R> __device__ __forceinline__ V3<R> mulT(const Rot<R>& r, V3<R> 
           r.m[0][2] * a.x + r.m[1][2] * a.y + r.m[2][2] * a.z};
 }
 
+// ---------------------------------------------------------------- fp32 pairs
+// sm_100's FP32x2 path: FADD2 / FMUL2 / FFMA2 perform two fp32 operations per
+// instruction, each half rounded exactly like the scalar instruction.  A
+// broadcast scalar, a swapped pair and a negated half are operand modifiers,
+// so pairing (x, y) halves the issue slots of 2-vector work.  Pairs live in
+// 64-bit registers: the halves of a loaded float4 / float2 are pairs already.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2pk(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float f2lo(f2_t r) {
+  float lo;
+  asm("mov.b64 {%0, _}, %1;" : "=f"(lo) : "l"(r));
+  return lo;
+}
+__device__ __forceinline__ float f2hi(f2_t r) {
+  float hi;
+  asm("mov.b64 {_, %0}, %1;" : "=f"(hi) : "l"(r));
+  return hi;
+}
+__device__ __forceinline__ f2_t bc2(float s) { return f2pk(s, s); }
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// fp32 rotation matrix packed for R v: column pairs (m0j, m1j), row 2 scalar.
+struct RotP {
+  f2_t c0, c1, c2;          // (m00, m10), (m01, m11), (m02, m12)
+  float m20, m21, m22;
+  float dd0, dd1, dd2;      // m_ii - 1, formed without cancellation
+};
+// Same formulas and operation order as rotation(): e.g. m10 = 2 (x y + w z),
+// dd0 = -2 (y^2 + z^2); pairs Q1 = (x, y), Q2 = (z, w) of the quaternion.
+__device__ __forceinline__ RotP rotation_p(float x, float y, float z, float w) {
+  RotP r;
+  const f2_t Q1 = f2pk(x, y);
+  const f2_t nyx = f2pk(-y, x);
+  // column 0: 2 (-(y y + z z), x y + w z)
+  const f2_t t0 = mul2(fma2(f2pk(-z, w), bc2(z), mul2(nyx, bc2(y))), bc2(2.f));
+  // column 1: 2 (x y - w z, -(x x + z z))
+  const f2_t t1 = mul2(fma2(f2pk(-w, -z), bc2(z), mul2(nyx, bc2(-x))), bc2(2.f));
+  // column 2: 2 (x z + w y, y z - w x); row 2: 2 (x z - w y, y z + w x)
+  const f2_t xzyz = mul2(Q1, bc2(z));
+  r.c2 = mul2(fma2(nyx, bc2(-w), xzyz), bc2(2.f));
+  const f2_t r2 = mul2(fma2(nyx, bc2(w), xzyz), bc2(2.f));
+  r.dd0 = f2lo(t0);
+  r.dd1 = f2hi(t1);
+  r.dd2 = -2.f * (x * x + y * y);
+  r.c0 = f2pk(1.f + r.dd0, f2hi(t0));
+  r.c1 = f2pk(f2lo(t1), 1.f + r.dd1);
+  r.m20 = f2lo(r2);
+  r.m21 = f2hi(r2);
+  r.m22 = 1.f + r.dd2;
+  return r;
+}
+// R a = a.x c0 + a.y c1 + a.z c2 (x, y packed)
+__device__ __forceinline__ V3<float> mul(const RotP& r, V3<float> a) {
+  const f2_t xy = fma2(r.c2, bc2(a.z), fma2(r.c1, bc2(a.y), mul2(r.c0, bc2(a.x))));
+  return {f2lo(xy), f2hi(xy), r.m20 * a.x + r.m21 * a.y + r.m22 * a.z};
+}
+// R^T a: one dot product per column
+__device__ __forceinline__ V3<float> mulT(const RotP& r, V3<float> a) {
+  return {f2lo(r.c0) * a.x + f2hi(r.c0) * a.y + r.m20 * a.z,
+          f2lo(r.c1) * a.x + f2hi(r.c1) * a.y + r.m21 * a.z,
+          f2lo(r.c2) * a.x + f2hi(r.c2) * a.y + r.m22 * a.z};
+}
+
 // Cyclic permutation Pi of reading R5: world -> bond frame of axis AX.
 template <int AX, class R> __device__ __forceinline__ V3<R> to_bond(V3<R> a) {
   if constexpr (AX == 0) return a;
@@ -149,6 +235,10 @@ template <int AX, class R> __device__ __forceinline__ V3<R> to_world(V3<R> a) {
 __device__ __forceinline__ float vx_atan2(float y, float x) { return atan2f(y, x); }
 __device__ __forceinline__ double vx_atan2(double y, double x) { return atan2(y, x); }
 __device__ __forceinline__ float vx_sqrt(float x) { return sqrtf(x); }
+// 1/sqrt(x) for renormalising a unit quaternion: fp32 uses the hardware
+// reciprocal square root (MUFU.RSQ, ~2 ulp: the factor is ~1 +- 1e-7 anyway)
+__device__ __forceinline__ float vx_rnorm(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double vx_rnorm(double x) { return 1.0 / sqrt(x); }
 __device__ __forceinline__ double vx_sqrt(double x) { return sqrt(x); }
 __device__ __forceinline__ void vx_sincos(float a, float* s, float* c) { sincosf(a, s, c); }
 __device__ __forceinline__ void vx_sincos(double a, double* s, double* c) { sincos(a, s, c); }

@@ -206,8 +206,9 @@ __device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
   R qx = qa.w * qb.x - qa.x * qb.w - qa.y * qb.z + qa.z * qb.y;
   R qy = qa.w * qb.y + qa.x * qb.z - qa.y * qb.w - qa.z * qb.x;
   R qz = qa.w * qb.z - qa.x * qb.y + qa.y * qb.x - qa.z * qb.w;
-  if (qw < R(0)) { qw = -qw; qx = -qx; qy = -qy; qz = -qz; }
-  const V3<R> th = to_bond<AX>(rotvec_scale(qw, qx, qy, qz) * mk(qx, qy, qz));
+  // w < 0: theta of -q_rel (the same rotation); the sign folds into the scale
+  const R sg = qw < R(0) ? R(-1) : R(1);
+  const V3<R> th = to_bond<AX>((sg * rotvec_scale(fabs(qw), qx, qy, qz)) * mk(qx, qy, qz));
 
   // Eq. 40: X2 = d_x - L_T with L_T = l (1 + alpha_mean dT)
   const R X2 = dv.x - l * c.alpha_mean * dT;
@@ -230,17 +231,92 @@ __device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
   if constexpr (AX == 0) r.x += l;
   else if constexpr (AX == 1) r.y += l;
   else r.z += l;
+#ifndef VX_EXP_NODAMP
   const V3<R> dV = Vb - Va;
   const V3<R> rw = cross(r, wa + wb);
   const V3<R> dw = wb - wa;
   Fa = Fa + c.ct2 * dV + c.ct4 * rw;
   Ma = Ma + c.cr2 * dw;
   Mbw = Mbw - c.cr2 * dw;
+#endif
+}
+
+// fp32 bond: the same operations in the same order as the generic bond_eval,
+// with 2-vector work on the FP32x2 path (vx_common.cuh): the relative
+// quaternion as two pair products (qx, qy), (qz, qw); rotations back to the
+// world frame by column pairs; velocities and the damping sums paired.
+// Pairs used: (u, P).xy from the float4 loads, (phi_y, phi_z) from the
+// float2 load, (x, y) / (z, w) of each quaternion.
+template <int AX>
+__device__ __forceinline__ void bond_eval(const Dev<float>& d, const RotP& Ra, const float4& qa,
+                                          V3<float> ua, V3<float> Va, V3<float> wa, int mat_a,
+                                          const VS<float>& b, float dT, V3<float>& Fa,
+                                          V3<float>& Ma, V3<float>& Mbw) {
+  const float4& pb = b.p;
+  const float4& qb = b.q;
+  const int mat_b = meta_of(pb.w) & M_MAT;
+  const PairC<float> c = d.pair[mat_a * d.nmat + mat_b];
+  const float l = d.l;
+
+  const f2_t duxy = sub2(f2pk(pb.x, pb.y), f2pk(ua.x, ua.y));
+  const V3<float> du = mk(f2lo(duxy), f2hi(duxy), pb.z - ua.z);
+  V3<float> t;  // R^T e_AX - e_AX = row AX of (R - I)
+  if constexpr (AX == 0) t = mk(Ra.dd0, f2lo(Ra.c1), f2lo(Ra.c2));
+  else if constexpr (AX == 1) t = mk(f2hi(Ra.c0), Ra.dd1, f2hi(Ra.c2));
+  else t = mk(Ra.m20, Ra.m21, Ra.dd2);
+  const V3<float> dv = to_bond<AX>(l * t + mulT(Ra, du));
+
+  // q_rel = q_a* q_b:
+  //   (qx, qy) = aw (bx, by) + ax (-bw, bz) - ay (bz, bw) - az (-by, bx)
+  //   (qz, qw) = aw (bz, bw) + ax (-by, bx) + ay (bx, by) + az (-bw, bz)
+  const f2_t B1 = f2pk(qb.x, qb.y), B2 = f2pk(qb.z, qb.w);
+  const f2_t nB1 = f2pk(-qb.y, qb.x), nB2 = f2pk(-qb.w, qb.z);
+  const f2_t qxy = fma2(bc2(-qa.z), nB1, fma2(bc2(-qa.y), B2, fma2(bc2(qa.x), nB2,
+                                                                   mul2(bc2(qa.w), B1))));
+  const f2_t qzw = fma2(bc2(qa.z), nB2, fma2(bc2(qa.y), B1, fma2(bc2(qa.x), nB1,
+                                                                 mul2(bc2(qa.w), B2))));
+  const float qx = f2lo(qxy), qy = f2hi(qxy), qz = f2lo(qzw), qw = f2hi(qzw);
+  const float kth = (qw < 0.f ? -1.f : 1.f) * rotvec_scale(fabsf(qw), qx, qy, qz);
+  const f2_t thxy = mul2(bc2(kth), qxy);
+  const V3<float> th = to_bond<AX>(mk(f2lo(thxy), f2hi(thxy), kth * qz));
+
+  const float X2 = dv.x - l * c.alpha_mean * dT;
+  const float Y2 = dv.y, Z2 = dv.z;
+  const V3<float> fa = mk(c.a1 * X2, c.b1 * Y2 - c.b2 * th.z, c.b1 * Z2 + c.b2 * th.y);
+  const V3<float> ma = mk(c.a2 * th.x, -c.b2 * Z2 - c.b3 * th.y, c.b2 * Y2 - c.b3 * th.z);
+  const V3<float> mbl = mk(-c.a2 * th.x, -c.b2 * Z2 - 2.f * c.b3 * th.y,
+                           c.b2 * Y2 - 2.f * c.b3 * th.z);
+  Fa = mul(Ra, to_world<AX>(fa));
+  Ma = mul(Ra, to_world<AX>(ma));
+  Mbw = mul(Ra, to_world<AX>(mbl));
+
+  // Eq. 33-35 (see the generic bond_eval)
+  const f2_t Vbxy = mul2(bc2(c.inv_m_b), f2pk(b.mo.x, b.mo.y));
+  const float Vbz = c.inv_m_b * b.mo.z;
+  const f2_t wbyz = mul2(bc2(c.inv_I_b), f2pk(b.an.x, b.an.y));
+  const float wbx = c.inv_I_b * b.mo.w;
+  V3<float> r = du;
+  if constexpr (AX == 0) r.x += l;
+  else if constexpr (AX == 1) r.y += l;
+  else r.z += l;
+  const f2_t dVxy = sub2(Vbxy, f2pk(Va.x, Va.y));
+  const float dVz = Vbz - Va.z;
+  const f2_t syz = add2(f2pk(wa.y, wa.z), wbyz);
+  const V3<float> rw = cross(r, mk(wa.x + wbx, f2lo(syz), f2hi(syz)));
+  const f2_t dwyz = sub2(wbyz, f2pk(wa.y, wa.z));
+  const float dwx = wbx - wa.x;
+  const f2_t Fxy = fma2(bc2(c.ct4), f2pk(rw.x, rw.y), fma2(bc2(c.ct2), dVxy, f2pk(Fa.x, Fa.y)));
+  Fa = mk(f2lo(Fxy), f2hi(Fxy), fmaf(c.ct4, rw.z, fmaf(c.ct2, dVz, Fa.z)));
+  Ma = mk(fmaf(c.cr2, dwx, Ma.x), fmaf(c.cr2, f2lo(dwyz), Ma.y), fmaf(c.cr2, f2hi(dwyz), Ma.z));
+  Mbw = mk(fmaf(-c.cr2, dwx, Mbw.x), fmaf(-c.cr2, f2lo(dwyz), Mbw.y),
+           fmaf(-c.cr2, f2hi(dwyz), Mbw.z));
 }
 
 // The parts of voxel a that every bond of a shares.
+template <class R> struct RotOf { using T = Rot<R>; };
+template <> struct RotOf<float> { using T = RotP; };
 template <class R> struct AFrame {
-  Rot<R> Ra;
+  typename RotOf<R>::T Ra;
   V3<R> ua, Va, wa;
   int mat;
 };
@@ -249,10 +325,18 @@ template <class R> __device__ __forceinline__ AFrame<R> a_frame(const Dev<R>& d,
   const uint32_t meta = meta_of(a.p.w);
   f.mat = meta & M_MAT;
   const MatC<R>& M = d.mat[f.mat];
-  f.Ra = rotation(a.q.w, a.q.x, a.q.y, a.q.z);
   f.ua = mk(a.p.x, a.p.y, a.p.z);
-  f.Va = M.inv_m * mk(a.mo.x, a.mo.y, a.mo.z);
-  f.wa = M.inv_I * mk(a.mo.w, a.an.x, a.an.y);
+  if constexpr (sizeof(R) == 4) {
+    f.Ra = rotation_p(a.q.x, a.q.y, a.q.z, a.q.w);
+    const f2_t vxy = mul2(bc2(M.inv_m), f2pk(a.mo.x, a.mo.y));
+    const f2_t wyz = mul2(bc2(M.inv_I), f2pk(a.an.x, a.an.y));
+    f.Va = mk(f2lo(vxy), f2hi(vxy), M.inv_m * a.mo.z);
+    f.wa = mk(M.inv_I * a.mo.w, f2lo(wyz), f2hi(wyz));
+  } else {
+    f.Ra = rotation(a.q.w, a.q.x, a.q.y, a.q.z);
+    f.Va = M.inv_m * mk(a.mo.x, a.mo.y, a.mo.z);
+    f.wa = M.inv_I * mk(a.mo.w, a.an.x, a.an.y);
+  }
   return f;
 }
 
@@ -398,7 +482,7 @@ __device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, const VS
   R qx = dw * q.x + dx * q.w + dy * q.z - dz * q.y;
   R qy = dw * q.y - dx * q.z + dy * q.w + dz * q.x;
   R qz = dw * q.z + dx * q.y - dy * q.x + dz * q.w;
-  const R qi = R(1) / vx_sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+  const R qi = vx_rnorm(qw * qw + qx * qx + qy * qy + qz * qz);
   qw = qw * qi; qx = qx * qi; qy = qy * qi; qz = qz * qi;
   const uint32_t nmeta = latch ? (meta | M_LATCH) : (meta & ~M_LATCH);
   st_stream(opos + id, R4{u.x, u.y, u.z, meta_as(R(0), nmeta)});
