@@ -164,8 +164,8 @@ template <class R> __device__ __forceinline__ R rotvec_scale(R w, R x, R y, R z)
 // (P:189), Eq. 13-24 sign-fixed and negated (R1, R3), back to world,
 // plus local damping (Eq. 33-35, R10, R11).  Shared by K3 and the fused step.
 template <class R> struct VS {   // one voxel's state as loaded
-  typename VT<R>::R4 p, q, mo;   // (u, meta), quaternion (x,y,z,w), (P, phi.x)
-  typename VT<R>::R2 an;         // (phi.y, phi.z)
+  typename VT<R>::R4 p, q, mo;   // (u, meta), quaternion (x,y,z,w), (P, phi.z)
+  typename VT<R>::R2 an;         // (phi.x, phi.y)
 };
 template <class R>
 __device__ __forceinline__ VS<R> ld_vs(const typename VT<R>::R4* __restrict__ pos,
@@ -226,7 +226,7 @@ __device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
   //   w_r = w_b - w_avg = (w_b - w_a)/2
   // and c_t/2, c_t/4, c_r/2 come from the pair table (exact power-of-2 scalings).
   const V3<R> Vb = c.inv_m_b * mk(b.mo.x, b.mo.y, b.mo.z);
-  const V3<R> wb = c.inv_I_b * mk(b.mo.w, b.an.x, b.an.y);
+  const V3<R> wb = c.inv_I_b * mk(b.an.x, b.an.y, b.mo.w);
   V3<R> r = du;
   if constexpr (AX == 0) r.x += l;
   else if constexpr (AX == 1) r.y += l;
@@ -245,7 +245,7 @@ __device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
 // with 2-vector work on the FP32x2 path (vx_common.cuh): the relative
 // quaternion as two pair products (qx, qy), (qz, qw); rotations back to the
 // world frame by column pairs; velocities and the damping sums paired.
-// Pairs used: (u, P).xy from the float4 loads, (phi_y, phi_z) from the
+// Pairs used: (u, P).xy from the float4 loads, (phi_x, phi_y) from the
 // float2 load, (x, y) / (z, w) of each quaternion.
 template <int AX>
 __device__ __forceinline__ void bond_eval(const Dev<float>& d, const RotP& Ra, const float4& qa,
@@ -293,23 +293,25 @@ __device__ __forceinline__ void bond_eval(const Dev<float>& d, const RotP& Ra, c
   // Eq. 33-35 (see the generic bond_eval)
   const f2_t Vbxy = mul2(bc2(c.inv_m_b), f2pk(b.mo.x, b.mo.y));
   const float Vbz = c.inv_m_b * b.mo.z;
-  const f2_t wbyz = mul2(bc2(c.inv_I_b), f2pk(b.an.x, b.an.y));
-  const float wbx = c.inv_I_b * b.mo.w;
+  const f2_t wbxy = mul2(bc2(c.inv_I_b), f2pk(b.an.x, b.an.y));
+  const float wbz = c.inv_I_b * b.mo.w;
   V3<float> r = du;
   if constexpr (AX == 0) r.x += l;
   else if constexpr (AX == 1) r.y += l;
   else r.z += l;
+  const f2_t waxy = f2pk(wa.x, wa.y);
   const f2_t dVxy = sub2(Vbxy, f2pk(Va.x, Va.y));
   const float dVz = Vbz - Va.z;
-  const f2_t syz = add2(f2pk(wa.y, wa.z), wbyz);
-  const V3<float> rw = cross(r, mk(wa.x + wbx, f2lo(syz), f2hi(syz)));
-  const f2_t dwyz = sub2(wbyz, f2pk(wa.y, wa.z));
-  const float dwx = wbx - wa.x;
+  const f2_t sxy = add2(waxy, wbxy);
+  const V3<float> rw = cross(r, mk(f2lo(sxy), f2hi(sxy), wa.z + wbz));
+  const f2_t dwxy = sub2(wbxy, waxy);
+  const float dwz = wbz - wa.z;
   const f2_t Fxy = fma2(bc2(c.ct4), f2pk(rw.x, rw.y), fma2(bc2(c.ct2), dVxy, f2pk(Fa.x, Fa.y)));
   Fa = mk(f2lo(Fxy), f2hi(Fxy), fmaf(c.ct4, rw.z, fmaf(c.ct2, dVz, Fa.z)));
-  Ma = mk(fmaf(c.cr2, dwx, Ma.x), fmaf(c.cr2, f2lo(dwyz), Ma.y), fmaf(c.cr2, f2hi(dwyz), Ma.z));
-  Mbw = mk(fmaf(-c.cr2, dwx, Mbw.x), fmaf(-c.cr2, f2lo(dwyz), Mbw.y),
-           fmaf(-c.cr2, f2hi(dwyz), Mbw.z));
+  const f2_t Mxy = fma2(bc2(c.cr2), dwxy, f2pk(Ma.x, Ma.y));
+  Ma = mk(f2lo(Mxy), f2hi(Mxy), fmaf(c.cr2, dwz, Ma.z));
+  const f2_t Bxy = fma2(bc2(-c.cr2), dwxy, f2pk(Mbw.x, Mbw.y));
+  Mbw = mk(f2lo(Bxy), f2hi(Bxy), fmaf(-c.cr2, dwz, Mbw.z));
 }
 
 // The parts of voxel a that every bond of a shares.
@@ -329,13 +331,13 @@ template <class R> __device__ __forceinline__ AFrame<R> a_frame(const Dev<R>& d,
   if constexpr (sizeof(R) == 4) {
     f.Ra = rotation_p(a.q.x, a.q.y, a.q.z, a.q.w);
     const f2_t vxy = mul2(bc2(M.inv_m), f2pk(a.mo.x, a.mo.y));
-    const f2_t wyz = mul2(bc2(M.inv_I), f2pk(a.an.x, a.an.y));
+    const f2_t wxy = mul2(bc2(M.inv_I), f2pk(a.an.x, a.an.y));
     f.Va = mk(f2lo(vxy), f2hi(vxy), M.inv_m * a.mo.z);
-    f.wa = mk(M.inv_I * a.mo.w, f2lo(wyz), f2hi(wyz));
+    f.wa = mk(f2lo(wxy), f2hi(wxy), M.inv_I * a.mo.w);
   } else {
     f.Ra = rotation(a.q.w, a.q.x, a.q.y, a.q.z);
     f.Va = M.inv_m * mk(a.mo.x, a.mo.y, a.mo.z);
-    f.wa = M.inv_I * mk(a.mo.w, a.an.x, a.an.y);
+    f.wa = M.inv_I * mk(a.an.x, a.an.y, a.mo.w);
   }
   return f;
 }
@@ -374,11 +376,8 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 4 : 2) k_bonds(Dev<R> d,
 }
 
 // ------------------------------------------------------------------ K4 integrate
-// Rotation increment below this squared angle uses the series of cos(a/2) and
-// sin(a/2)/a through a^6 (next term < 1e-17 relative at the cut).
-template <class R> struct IncCut;
-template <> struct IncCut<float> { static constexpr float a2 = 0.05f * 0.05f; };
-template <> struct IncCut<double> { static constexpr double a2 = 0.01 * 0.01; };
+// Rotation increment below IncCut's squared angle uses the series of cos(a/2)
+// and sin(a/2)/a through a^6 (next term < 1e-17 relative at the cut).
 
 // Stores of the new state are never re-read by the same kernel: evict-first.
 __device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
@@ -389,6 +388,118 @@ __device__ __forceinline__ void st_stream(double4* p, double4 v) {
   __stcs(q + 1, make_double2(v.z, v.w));
 }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
+
+// Eq. 27-30 and the store of S_{n+1}: P += F dt, D += (P/m) dt, phi += M dt,
+// q <- normalize(quat(th) (x) q), quat(th) = (cos(a/2), sin(a/2) th/a),
+// th = (phi/I) dt, a = |th|; returns |V| for the motion budget.
+template <class R> struct IncCut;
+template <> struct IncCut<float> { static constexpr float a2 = 0.05f * 0.05f; };
+template <> struct IncCut<double> { static constexpr double a2 = 0.01 * 0.01; };
+// cos(a/2) and sin(a/2)/a of the per-step rotation increment
+template <class R> __device__ __forceinline__ void inc_coeffs(R a2, R& dw, R& ks) {
+  if (a2 < IncCut<R>::a2) {   // per-step angles are tiny: Taylor series, no sincos
+    dw = R(1) - a2 * (R(1) / R(8) - a2 * (R(1) / R(384) - a2 * (R(1) / R(46080))));
+    ks = R(0.5) - a2 * (R(1) / R(48) - a2 * (R(1) / R(3840) - a2 * (R(1) / R(645120))));
+  } else {
+    const R a = vx_sqrt(a2);
+    R sh;
+    vx_sincos(R(0.5) * a, &sh, &dw);
+    ks = sh / a;
+  }
+}
+template <class R> __device__ __forceinline__ void flag_nonfinite(const Dev<R>& d, uint32_t id, R z,
+                                                                  const uint32_t* ext_of_local) {
+  if (!(z == R(0))) {
+    const unsigned long long code =
+        ((unsigned long long)d.clk->step << 32) | (unsigned long long)ext_of_local[id];
+    atomicMin(&d.clk->err, code);
+  }
+}
+template <class R, bool COLLIDE>
+__device__ __forceinline__ R integrate_store(const Dev<R>& d, uint32_t id, const VS<R>& s,
+                                             uint32_t nmeta, const MatC<R>& mc, V3<R> F, V3<R> M,
+                                             bool zero_lat, typename VT<R>::R4* __restrict__ opos,
+                                             typename VT<R>::R4* __restrict__ oquat,
+                                             typename VT<R>::R4* __restrict__ omom,
+                                             typename VT<R>::R2* __restrict__ oang,
+                                             const uint32_t* __restrict__ ext_of_local) {
+  using R4 = typename VT<R>::R4;
+  using R2 = typename VT<R>::R2;
+  const R4& p = s.p;
+  const R4& mo = s.mo;
+  V3<R> P = mk(mo.x, mo.y, mo.z) + d.dt * F;
+  if (zero_lat) { P.x = R(0); P.y = R(0); }
+  const V3<R> u = mk(p.x, p.y, p.z) + mc.dt_m * P;
+  const V3<R> phi = mk(s.an.x, s.an.y, mo.w) + d.dt * M;
+  const V3<R> th = mc.dt_I * phi;
+  R dw, ks;
+  inc_coeffs(dot(th, th), dw, ks);
+  const R dx = ks * th.x, dy = ks * th.y, dz = ks * th.z;
+  const R4& q = s.q;
+  R qw = dw * q.w - dx * q.x - dy * q.y - dz * q.z;
+  R qx = dw * q.x + dx * q.w + dy * q.z - dz * q.y;
+  R qy = dw * q.y - dx * q.z + dy * q.w + dz * q.x;
+  R qz = dw * q.z + dx * q.y - dy * q.x + dz * q.w;
+  const R qi = vx_rnorm(qw * qw + qx * qx + qy * qy + qz * qz);
+  qw = qw * qi; qx = qx * qi; qy = qy * qi; qz = qz * qi;
+  st_stream(opos + id, R4{u.x, u.y, u.z, meta_as(R(0), nmeta)});
+  st_stream(oquat + id, R4{qx, qy, qz, qw});
+  st_stream(omom + id, R4{P.x, P.y, P.z, phi.z});
+  st_stream(oang + id, R2{phi.x, phi.y});
+  // any NaN/Inf among the 13 values: x * 0 is NaN exactly for non-finite x
+  const R z0 = (u.x + u.y + u.z + qw + qx + qy + qz) * R(0);
+  const R z1 = (P.x + P.y + P.z + phi.x + phi.y + phi.z) * R(0);
+  flag_nonfinite(d, id, z0 + z1, ext_of_local);
+  return COLLIDE ? vx_sqrt(dot(P, P)) * mc.inv_m : R(0);
+}
+// fp32: the same steps with (x, y) of P, D, phi, th and the two halves
+// (x, y), (z, w) of the quaternion product on the FP32x2 path.
+//   (qx', qy') = dw (qx, qy) - dx (-qw, qz) + dy (qz, qw) + dz (-qy, qx)
+//   (qz', qw') = dw (qz, qw) - dx (-qy, qx) - dy (qx, qy) - dz (-qw, qz)
+template <bool COLLIDE>
+__device__ __forceinline__ float integrate_store_f32(const Dev<float>& d, uint32_t id, const VS<float>& s,
+                                                 uint32_t nmeta, const MatC<float>& mc, V3<float> F,
+                                                 V3<float> M, bool zero_lat, float4* __restrict__ opos,
+                                                 float4* __restrict__ oquat, float4* __restrict__ omom,
+                                                 float2* __restrict__ oang,
+                                                 const uint32_t* __restrict__ ext_of_local) {
+  const float4& p = s.p;
+  const float4& mo = s.mo;
+  f2_t Pxy = fma2(bc2(d.dt), f2pk(F.x, F.y), f2pk(mo.x, mo.y));
+  const float Pz = fmaf(d.dt, F.z, mo.z);
+  if (zero_lat) Pxy = 0ull;
+  const f2_t uxy = fma2(bc2(mc.dt_m), Pxy, f2pk(p.x, p.y));
+  const float uz = fmaf(mc.dt_m, Pz, p.z);
+  const f2_t phxy = fma2(bc2(d.dt), f2pk(M.x, M.y), f2pk(s.an.x, s.an.y));
+  const float phz = fmaf(d.dt, M.z, mo.w);
+  const f2_t thxy = mul2(bc2(mc.dt_I), phxy);
+  const float thx = f2lo(thxy), thy = f2hi(thxy), thz = mc.dt_I * phz;
+  float dw, ks;
+  inc_coeffs(thx * thx + thy * thy + thz * thz, dw, ks);
+  const f2_t dxy = mul2(bc2(ks), thxy);
+  const float dx = f2lo(dxy), dy = f2hi(dxy), dz = ks * thz;
+  const float4& q = s.q;
+  const f2_t Q1 = f2pk(q.x, q.y), Q2 = f2pk(q.z, q.w);
+  const f2_t nQ1 = f2pk(-q.y, q.x), nQ2 = f2pk(-q.w, q.z);
+  f2_t q1 = fma2(bc2(dz), nQ1, fma2(bc2(dy), Q2, fma2(bc2(-dx), nQ2, mul2(bc2(dw), Q1))));
+  f2_t q2 = fma2(bc2(-dz), nQ2, fma2(bc2(-dy), Q1, fma2(bc2(-dx), nQ1, mul2(bc2(dw), Q2))));
+  const f2_t nn = fma2(q1, q1, mul2(q2, q2));
+  const float qi = vx_rnorm(f2lo(nn) + f2hi(nn));
+  q1 = mul2(bc2(qi), q1);
+  q2 = mul2(bc2(qi), q2);
+  st_stream(opos + id, float4{f2lo(uxy), f2hi(uxy), uz, meta_as(0.f, nmeta)});
+  st_stream(oquat + id, float4{f2lo(q1), f2hi(q1), f2lo(q2), f2hi(q2)});
+  st_stream(omom + id, float4{f2lo(Pxy), f2hi(Pxy), Pz, phz});
+  st_stream(oang + id, float2{f2lo(phxy), f2hi(phxy)});
+  // any NaN/Inf among the 13 values: x * 0 is NaN exactly for non-finite x
+  const f2_t sxy = add2(add2(add2(add2(uxy, q1), q2), Pxy), phxy);
+  flag_nonfinite(d, id, (f2lo(sxy) + f2hi(sxy) + uz + Pz + phz) * 0.f, ext_of_local);
+  if constexpr (COLLIDE) {
+    const f2_t pp = mul2(Pxy, Pxy);
+    return vx_sqrt(f2lo(pp) + f2hi(pp) + Pz * Pz) * mc.inv_m;
+  }
+  return 0.f;
+}
 
 // After the slot sums (Eq. 25-26): external force, gravity, ground
 // damping (R12), contacts, floor + friction (R14, R15),
@@ -401,21 +512,31 @@ __device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, const VS
                                           typename VT<R>::R2* __restrict__ oang,
                                           const uint32_t* __restrict__ ext_of_local) {
   using R4 = typename VT<R>::R4;
-  using R2 = typename VT<R>::R2;
   const MatC<R> mc = d.mat[meta & M_MAT];
   const R4& p = s.p;
   const R4& mo = s.mo;
-  const R2& an = s.an;
   if (meta & M_EXT) {
     const R4 fe = d.fext[id];
     F = F + mk(fe.x, fe.y, fe.z);
   }
   F.z = F.z - mc.mg;
-  const V3<R> V = mc.inv_m * mk(mo.x, mo.y, mo.z);
-  const V3<R> w = mc.inv_I * mk(mo.w, an.x, an.y);
-  if (d.ground) {                                     // P:254, R12
-    F = F - mc.cgt * V;
-    M = M - mc.cgr * w;
+  V3<R> V;
+  if constexpr (sizeof(R) == 4) {
+    const f2_t vxy = mul2(bc2(mc.inv_m), f2pk(mo.x, mo.y));
+    V = mk(f2lo(vxy), f2hi(vxy), mc.inv_m * mo.z);
+    if (d.ground) {                                   // P:254, R12
+      const f2_t wxy = mul2(bc2(mc.inv_I), f2pk(s.an.x, s.an.y));
+      const f2_t fxy = fma2(bc2(-mc.cgt), vxy, f2pk(F.x, F.y));
+      const f2_t mxy = fma2(bc2(-mc.cgr), wxy, f2pk(M.x, M.y));
+      F = mk(f2lo(fxy), f2hi(fxy), fmaf(-mc.cgt, V.z, F.z));
+      M = mk(f2lo(mxy), f2hi(mxy), fmaf(-mc.cgr, mc.inv_I * mo.w, M.z));
+    }
+  } else {
+    V = mc.inv_m * mk(mo.x, mo.y, mo.z);
+    if (d.ground) {                                   // P:254, R12
+      F = F - mc.cgt * V;
+      M = M - mc.cgr * (mc.inv_I * mk(s.an.x, s.an.y, mo.w));
+    }
   }
   if constexpr (COLLIDE) {
     if (meta & M_SURF) {
@@ -458,46 +579,13 @@ __device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, const VS
       latch = false;
     }
   }
-  // Eq. 27-30
-  V3<R> P = mk(mo.x, mo.y, mo.z) + d.dt * F;
-  if (zero_lat) { P.x = R(0); P.y = R(0); }
-  const V3<R> u = mk(p.x, p.y, p.z) + mc.dt_m * P;
-  const V3<R> phi = mk(mo.w, an.x, an.y) + d.dt * M;
-  // q <- normalize(quat(th) (x) q), quat(th) = (cos(a/2), sin(a/2) th/a), a = |th|
-  const V3<R> th = mc.dt_I * phi;
-  const R a2 = dot(th, th);
-  R dw, ks;
-  if (a2 < IncCut<R>::a2) {   // per-step angles are tiny: Taylor series, no sincos
-    dw = R(1) - a2 * (R(1) / R(8) - a2 * (R(1) / R(384) - a2 * (R(1) / R(46080))));
-    ks = R(0.5) - a2 * (R(1) / R(48) - a2 * (R(1) / R(3840) - a2 * (R(1) / R(645120))));
-  } else {
-    const R a = vx_sqrt(a2);
-    R sh;
-    vx_sincos(R(0.5) * a, &sh, &dw);
-    ks = sh / a;
-  }
-  const R dx = ks * th.x, dy = ks * th.y, dz = ks * th.z;
-  const R4& q = s.q;
-  R qw = dw * q.w - dx * q.x - dy * q.y - dz * q.z;
-  R qx = dw * q.x + dx * q.w + dy * q.z - dz * q.y;
-  R qy = dw * q.y - dx * q.z + dy * q.w + dz * q.x;
-  R qz = dw * q.z + dx * q.y - dy * q.x + dz * q.w;
-  const R qi = vx_rnorm(qw * qw + qx * qx + qy * qy + qz * qz);
-  qw = qw * qi; qx = qx * qi; qy = qy * qi; qz = qz * qi;
   const uint32_t nmeta = latch ? (meta | M_LATCH) : (meta & ~M_LATCH);
-  st_stream(opos + id, R4{u.x, u.y, u.z, meta_as(R(0), nmeta)});
-  st_stream(oquat + id, R4{qx, qy, qz, qw});
-  st_stream(omom + id, R4{P.x, P.y, P.z, phi.x});
-  st_stream(oang + id, R2{phi.y, phi.z});
-  // any NaN/Inf among the 13 values: x * 0 is NaN exactly for non-finite x
-  const R z0 = (u.x + u.y + u.z + qw + qx + qy + qz) * R(0);
-  const R z1 = (P.x + P.y + P.z + phi.x + phi.y + phi.z) * R(0);
-  if (!(z0 + z1 == R(0))) {
-    const unsigned long long code =
-        ((unsigned long long)d.clk->step << 32) | (unsigned long long)ext_of_local[id];
-    atomicMin(&d.clk->err, code);
-  }
-  return COLLIDE ? vx_sqrt(dot(P, P)) * mc.inv_m : R(0);
+  if constexpr (sizeof(R) == 4)
+    return integrate_store_f32<COLLIDE>(d, id, s, nmeta, mc, F, M, zero_lat, opos, oquat, omom,
+                                        oang, ext_of_local);
+  else
+    return integrate_store<R, COLLIDE>(d, id, s, nmeta, mc, F, M, zero_lat, opos, oquat, omom,
+                                       oang, ext_of_local);
 }
 
 // Block max of |V| -> motion budget.  All threads of the block call it.
@@ -573,9 +661,36 @@ __global__ void __launch_bounds__(256) k_integrate(Dev<R> d, uint32_t beg, uint3
 // Halo: the +y bond of row j0-1 per plane and the +x bond of plane i0-1 per
 // segment are recomputed.  The slot sums and finish_voxel are K4's, in K4's
 // order, so the update is the two-kernel update.
-template <class R> struct Rec6 {   // (F_a, M_b): what the "b" side of a bond needs
+// (F_a, M_b): what the "b" side of a bond needs, stored as
+// (F.x, F.y, M.x, M.y, F.z, M.z) so each (x, y) is an aligned fp32 pair.
+template <class R> struct __align__(2 * sizeof(R)) Rec6 {
   R f[6];
 };
+template <class R> __device__ __forceinline__ Rec6<R> rec6(V3<R> F, V3<R> M) {
+  return Rec6<R>{{F.x, F.y, M.x, M.y, F.z, M.z}};
+}
+// Slot sums (Eq. 25-26): a -axis slot adds (-F_a, M_b) of its record, a
+// +axis slot (F_a, M_a) of the voxel's own bond.
+template <class R> __device__ __forceinline__ void slot_minus(V3<R>& F, V3<R>& M, const Rec6<R>& r) {
+  F = F - mk(r.f[0], r.f[1], r.f[4]);
+  M = M + mk(r.f[2], r.f[3], r.f[5]);
+}
+template <class R> __device__ __forceinline__ void slot_plus(V3<R>& F, V3<R>& M, V3<R> Fo, V3<R> Mo) {
+  F = F + Fo;
+  M = M + Mo;
+}
+__device__ __forceinline__ void slot_minus(V3<float>& F, V3<float>& M, const Rec6<float>& r) {
+  const f2_t fxy = sub2(f2pk(F.x, F.y), f2pk(r.f[0], r.f[1]));
+  const f2_t mxy = add2(f2pk(M.x, M.y), f2pk(r.f[2], r.f[3]));
+  F = mk(f2lo(fxy), f2hi(fxy), F.z - r.f[4]);
+  M = mk(f2lo(mxy), f2hi(mxy), M.z + r.f[5]);
+}
+__device__ __forceinline__ void slot_plus(V3<float>& F, V3<float>& M, V3<float> Fo, V3<float> Mo) {
+  const f2_t fxy = add2(f2pk(F.x, F.y), f2pk(Fo.x, Fo.y));
+  const f2_t mxy = add2(f2pk(M.x, M.y), f2pk(Mo.x, Mo.y));
+  F = mk(f2lo(fxy), f2hi(fxy), F.z + Fo.z);
+  M = mk(f2lo(mxy), f2hi(mxy), M.z + Mo.z);
+}
 template <class R> struct FusedArgs {
   typename VT<R>::R4* opos;
   typename VT<R>::R4* oquat;
@@ -625,7 +740,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
           const AFrame<R> f = a_frame(d, va);
           V3<R> Fa, Ma, Mb;
           bond_eval<0>(d, f.Ra, va.q, f.ua, f.Va, f.wa, f.mat, vb, dT, Fa, Ma, Mb);
-          r = Rec6<R>{{Fa.x, Fa.y, Fa.z, Mb.x, Mb.y, Mb.z}};
+          r = rec6(Fa, Mb);
         }
       }
       xrec[(size_t)(j - j0) * nzb + k] = r;
@@ -642,7 +757,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
           const AFrame<R> f = a_frame(d, vh);
           V3<R> Fa, Ma, Mb;
           bond_eval<1>(d, f.Ra, vh.q, f.ua, f.Va, f.wa, f.mat, va, dT, Fa, Ma, Mb);
-          ry = Rec6<R>{{Fa.x, Fa.y, Fa.z, Mb.x, Mb.y, Mb.z}};
+          ry = rec6(Fa, Mb);
         }
       }
     }
@@ -664,25 +779,24 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
         if (meta & nb_bit(3)) bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nxt, dT, FY, MY, BY);
       }
       Rec6<R>* zr = zrec + (size_t)par * nzb;
-      if (act) zr[k] = Rec6<R>{{FZ.x, FZ.y, FZ.z, BZ.x, BZ.y, BZ.z}};
+      if (act) zr[k] = rec6(FZ, BZ);
       // K4's slot order -x, +x, -y, +y | -z, +z: the first four before the barrier
       Rec6<R>& xr = xrec[(size_t)(j - j0) * nzb + k];
       V3<R> F = mk(R(0), R(0), R(0)), M = F;
-      if (meta & nb_bit(0)) { F = F - mk(xr.f[0], xr.f[1], xr.f[2]); M = M + mk(xr.f[3], xr.f[4], xr.f[5]); }
-      if (meta & nb_bit(1)) { F = F + FX; M = M + MX; }
-      if (meta & nb_bit(2)) { F = F - mk(ry.f[0], ry.f[1], ry.f[2]); M = M + mk(ry.f[3], ry.f[4], ry.f[5]); }
-      if (meta & nb_bit(3)) { F = F + FY; M = M + MY; }
-      if (act && (meta & M_FILLED)) xr = Rec6<R>{{FX.x, FX.y, FX.z, BX.x, BX.y, BX.z}};
-      ry = Rec6<R>{{FY.x, FY.y, FY.z, BY.x, BY.y, BY.z}};
+      if (meta & nb_bit(0)) { slot_minus(F, M, xr); }
+      if (meta & nb_bit(1)) slot_plus(F, M, FX, MX);
+      if (meta & nb_bit(2)) { slot_minus(F, M, ry); }
+      if (meta & nb_bit(3)) slot_plus(F, M, FY, MY);
+      if (act && (meta & M_FILLED)) xr = rec6(FX, BX);
+      ry = rec6(FY, BY);
       __syncthreads();
       if (!act) return;
       if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
         if (meta & nb_bit(4)) {
           const Rec6<R>& z = zr[k - 1];
-          F = F - mk(z.f[0], z.f[1], z.f[2]);
-          M = M + mk(z.f[3], z.f[4], z.f[5]);
+          slot_minus(F, M, z);
         }
-        if (meta & nb_bit(5)) { F = F + FZ; M = M + MZ; }
+        if (meta & nb_bit(5)) slot_plus(F, M, FZ, MZ);
         const R v = finish_voxel<R, COLLIDE>(d, id, cur, meta, F, M, a.opos, a.oquat, a.omom,
                                              a.oang, a.ext_of_local);
         vmax = fmax(vmax, v);
@@ -839,7 +953,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R
           const AFrame<R> f = a_frame(d, va);
           V3<R> Fa, Ma, Mb;
           bond_eval<0>(d, f.Ra, va.q, f.ua, f.Va, f.wa, f.mat, vb, dT, Fa, Ma, Mb);
-          r = Rec6<R>{{Fa.x, Fa.y, Fa.z, Mb.x, Mb.y, Mb.z}};
+          r = rec6(Fa, Mb);
         }
       }
       xrec[(size_t)(j - j0) * nzb + k] = r;
@@ -858,7 +972,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R
           const AFrame<R> f = a_frame(d, vh);
           V3<R> Fa, Ma, Mb;
           bond_eval<1>(d, f.Ra, vh.q, f.ua, f.Va, f.wa, f.mat, va, dT, Fa, Ma, Mb);
-          ry = Rec6<R>{{Fa.x, Fa.y, Fa.z, Mb.x, Mb.y, Mb.z}};
+          ry = rec6(Fa, Mb);
         }
       }
     }
@@ -884,25 +998,24 @@ __global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R
         if (meta & nb_bit(3)) bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nxt, dT, FY, MY, BY);
       }
       Rec6<R>* zr = zrec + (size_t)((j - j0) & 1) * nzb;
-      if (act) zr[k] = Rec6<R>{{FZ.x, FZ.y, FZ.z, BZ.x, BZ.y, BZ.z}};
+      if (act) zr[k] = rec6(FZ, BZ);
       Rec6<R>& xr = xrec[(size_t)(j - j0) * nzb + k];
       V3<R> F = mk(R(0), R(0), R(0)), M = F;
-      if (meta & nb_bit(0)) { F = F - mk(xr.f[0], xr.f[1], xr.f[2]); M = M + mk(xr.f[3], xr.f[4], xr.f[5]); }
-      if (meta & nb_bit(1)) { F = F + FX; M = M + MX; }
-      if (meta & nb_bit(2)) { F = F - mk(ry.f[0], ry.f[1], ry.f[2]); M = M + mk(ry.f[3], ry.f[4], ry.f[5]); }
-      if (meta & nb_bit(3)) { F = F + FY; M = M + MY; }
-      if (act && (meta & M_FILLED)) xr = Rec6<R>{{FX.x, FX.y, FX.z, BX.x, BX.y, BX.z}};
-      ry = Rec6<R>{{FY.x, FY.y, FY.z, BY.x, BY.y, BY.z}};
+      if (meta & nb_bit(0)) { slot_minus(F, M, xr); }
+      if (meta & nb_bit(1)) slot_plus(F, M, FX, MX);
+      if (meta & nb_bit(2)) { slot_minus(F, M, ry); }
+      if (meta & nb_bit(3)) slot_plus(F, M, FY, MY);
+      if (act && (meta & M_FILLED)) xr = rec6(FX, BX);
+      ry = rec6(FY, BY);
       __syncthreads();   // z records visible; the x-row slot of row j may be refilled
       if (hasx) ++xe;
       if (act) {
         if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
           if (meta & nb_bit(4)) {
             const Rec6<R>& z = zr[k - 1];
-            F = F - mk(z.f[0], z.f[1], z.f[2]);
-            M = M + mk(z.f[3], z.f[4], z.f[5]);
+            slot_minus(F, M, z);
           }
-          if (meta & nb_bit(5)) { F = F + FZ; M = M + MZ; }
+          if (meta & nb_bit(5)) slot_plus(F, M, FZ, MZ);
           const R v = finish_voxel<R, COLLIDE>(d, id, cur, meta, F, M, a.opos, a.oquat, a.omom,
                                                a.oang, a.ext_of_local);
           vmax = fmax(vmax, v);
@@ -1183,7 +1296,7 @@ __global__ void k_scatter_state(Dev<R> d, const long long* box_of_ext, long long
   R4 mo = d.mom[li];
   R2 an = d.ang[li];
   if (lin) { mo.x = (R)lin[3 * e]; mo.y = (R)lin[3 * e + 1]; mo.z = (R)lin[3 * e + 2]; }
-  if (ang) { mo.w = (R)ang[3 * e]; an.x = (R)ang[3 * e + 1]; an.y = (R)ang[3 * e + 2]; }
+  if (ang) { an.x = (R)ang[3 * e]; an.y = (R)ang[3 * e + 1]; mo.w = (R)ang[3 * e + 2]; }
   d.mom[li] = mo;
   d.ang[li] = an;
 }
@@ -1205,7 +1318,7 @@ __global__ void k_pack_box(Dev<R> d, uint32_t beg, uint32_t end, long long box_b
   double v[14] = {site(ox, l, i) + (double)p.x, site(oy, l, j) + (double)p.y,
                   site(oz, l, k) + (double)p.z, (double)q.w, (double)q.x,
                   (double)q.y, (double)q.z, (double)mo.x, (double)mo.y, (double)mo.z,
-                  (double)mo.w, (double)an.x, (double)an.y,
+                  (double)an.x, (double)an.y, (double)mo.w,
                   (meta_of(p.w) & M_LATCH) ? 1.0 : 0.0};
 #pragma unroll
   for (int c = 0; c < 14; ++c) out[c * nbox + g] = v[c];
@@ -1245,7 +1358,7 @@ __global__ void k_read_ids(Dev<R> d, const long long* lids, const long long* gid
   pos[3 * e + 2] = site(oz, l, k) + (double)p.z;
   quat[4 * e] = q.w; quat[4 * e + 1] = q.x; quat[4 * e + 2] = q.y; quat[4 * e + 3] = q.z;
   lin[3 * e] = mo.x; lin[3 * e + 1] = mo.y; lin[3 * e + 2] = mo.z;
-  ang[3 * e] = mo.w; ang[3 * e + 1] = an.x; ang[3 * e + 2] = an.y;
+  ang[3 * e] = an.x; ang[3 * e + 1] = an.y; ang[3 * e + 2] = mo.w;
   latch[e] = (meta_of(p.w) & M_LATCH) ? 1 : 0;
 }
 
