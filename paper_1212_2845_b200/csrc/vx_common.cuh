@@ -183,6 +183,7 @@ struct RotP {
   f2_t c0, c1, c2;          // (m00, m10), (m01, m11), (m02, m12)
   float m20, m21, m22;
   float dd0, dd1, dd2;      // m_ii - 1, formed without cancellation
+  f2_t pax, paz;            // (-x, x), (z, -z): sign pairs of q for q* (x) q_b
 };
 // Same formulas and operation order as rotation(): e.g. m10 = 2 (x y + w z),
 // dd0 = -2 (y^2 + z^2); pairs Q1 = (x, y), Q2 = (z, w) of the quaternion.
@@ -201,8 +202,10 @@ __device__ __forceinline__ RotP rotation_p(float x, float y, float z, float w) {
   r.dd0 = f2lo(t0);
   r.dd1 = f2hi(t1);
   r.dd2 = -2.f * (x * x + y * y);
-  r.c0 = f2pk(1.f + r.dd0, f2hi(t0));
-  r.c1 = f2pk(f2lo(t1), 1.f + r.dd1);
+  r.c0 = add2(t0, f2pk(1.f, 0.f));
+  r.c1 = add2(t1, f2pk(0.f, 1.f));
+  r.pax = f2pk(-x, x);
+  r.paz = f2pk(z, -z);
   r.m20 = f2lo(r2);
   r.m21 = f2hi(r2);
   r.m22 = 1.f + r.dd2;

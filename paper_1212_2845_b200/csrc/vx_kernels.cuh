@@ -266,15 +266,15 @@ __device__ __forceinline__ void bond_eval(const Dev<float>& d, const RotP& Ra, c
   else t = mk(Ra.m20, Ra.m21, Ra.dd2);
   const V3<float> dv = to_bond<AX>(l * t + mulT(Ra, du));
 
-  // q_rel = q_a* q_b:
-  //   (qx, qy) = aw (bx, by) + ax (-bw, bz) - ay (bz, bw) - az (-by, bx)
-  //   (qz, qw) = aw (bz, bw) + ax (-by, bx) + ay (bx, by) + az (-bw, bz)
+  // q_rel = q_a* q_b, with the swapped pairs (by, bx), (bw, bz) and the
+  // per-voxel sign pairs (-ax, ax), (az, -az):
+  //   (qx, qy) = aw (bx, by) + (-ax, ax) (bw, bz) - ay (bz, bw) + (az, -az) (by, bx)
+  //   (qz, qw) = aw (bz, bw) + (-ax, ax) (by, bx) + ay (bx, by) - (az, -az) (bw, bz)
   const f2_t B1 = f2pk(qb.x, qb.y), B2 = f2pk(qb.z, qb.w);
-  const f2_t nB1 = f2pk(-qb.y, qb.x), nB2 = f2pk(-qb.w, qb.z);
-  const f2_t qxy = fma2(bc2(-qa.z), nB1, fma2(bc2(-qa.y), B2, fma2(bc2(qa.x), nB2,
-                                                                   mul2(bc2(qa.w), B1))));
-  const f2_t qzw = fma2(bc2(qa.z), nB2, fma2(bc2(qa.y), B1, fma2(bc2(qa.x), nB1,
-                                                                 mul2(bc2(qa.w), B2))));
+  const f2_t S1 = f2pk(qb.y, qb.x), S2 = f2pk(qb.w, qb.z);
+  const f2_t qxy = fma2(Ra.paz, S1, fma2(bc2(-qa.y), B2, fma2(Ra.pax, S2, mul2(bc2(qa.w), B1))));
+  const f2_t qzw = fma2(Ra.paz, sub2(0ull, S2), fma2(bc2(qa.y), B1, fma2(Ra.pax, S1,
+                                                                        mul2(bc2(qa.w), B2))));
   const float qx = f2lo(qxy), qy = f2hi(qxy), qz = f2lo(qzw), qw = f2hi(qzw);
   const float kth = (qw < 0.f ? -1.f : 1.f) * rotvec_scale(fabsf(qw), qx, qy, qz);
   const f2_t thxy = mul2(bc2(kth), qxy);
