@@ -575,6 +575,11 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
     VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     VX_CUDA(cudaFuncSetAttribute(k_step_fused_tma<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     VX_CUDA(cudaFuncSetAttribute(k_step_fused_tma<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    if (const char* e = std::getenv("VX_CARVEOUT")) {   // experiment: smem carveout percent
+      const int pct = std::atoi(e);
+      VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+      VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    }
     h->fused_smem_set[pi] = true;
   }
   const unsigned grid = (unsigned)(a.ntiles_y * segs);

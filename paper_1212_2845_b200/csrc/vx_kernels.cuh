@@ -704,15 +704,34 @@ template <class R> struct FusedArgs {
   int nplanes;      // planes in the local box
 };
 
+// Thread k's +z neighbour is thread k+1's own voxel: a warp shuffle of its
+// registers; lane 31 takes it from the next warp's lane 0 through shared
+// memory (written before the previous row's barrier).
+template <class R> __device__ __forceinline__ VS<R> vs_shfl_down(const VS<R>& s) {
+  constexpr unsigned F = 0xffffffffu;
+  VS<R> o;
+  o.p.x = __shfl_down_sync(F, s.p.x, 1); o.p.y = __shfl_down_sync(F, s.p.y, 1);
+  o.p.z = __shfl_down_sync(F, s.p.z, 1); o.p.w = __shfl_down_sync(F, s.p.w, 1);
+  o.q.x = __shfl_down_sync(F, s.q.x, 1); o.q.y = __shfl_down_sync(F, s.q.y, 1);
+  o.q.z = __shfl_down_sync(F, s.q.z, 1); o.q.w = __shfl_down_sync(F, s.q.w, 1);
+  o.mo.x = __shfl_down_sync(F, s.mo.x, 1); o.mo.y = __shfl_down_sync(F, s.mo.y, 1);
+  o.mo.z = __shfl_down_sync(F, s.mo.z, 1); o.mo.w = __shfl_down_sync(F, s.mo.w, 1);
+  o.an.x = __shfl_down_sync(F, s.an.x, 1); o.an.y = __shfl_down_sync(F, s.an.y, 1);
+  return o;
+}
+
 template <class R, bool COLLIDE>
 __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a) {
   using R4 = typename VT<R>::R4;
   using R2 = typename VT<R>::R2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nzb = blockDim.x;
-  // shared: xrec[ty][nzb], zrec[2][nzb] (Rec6)
+  // shared: xrec[ty][nzb], zrec[2][nzb] (Rec6), edge[2][nzb / 32] (VS: lane 0's
+  // next-row voxel for lane 31 of the warp below)
   Rec6<R>* xrec = reinterpret_cast<Rec6<R>*>(smem_raw);
   Rec6<R>* zrec = xrec + (size_t)a.ty * nzb;
+  VS<R>* edge = reinterpret_cast<VS<R>*>(zrec + 2 * (size_t)nzb);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = nzb >> 5;
 
   const int k = threadIdx.x;
   const bool act = k < (int)d.nz;
@@ -768,9 +787,13 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
       const uint32_t id = idx(i, j);
       if (act && (j + 1 < j1 || (meta & nb_bit(3))))
         nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
-      VS<R> vx, vz;
+      VS<R> vx;
       if (meta & nb_bit(1)) vx = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + sx);
-      if (meta & nb_bit(5)) vz = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + 1);   // L1: this row
+      VS<R> vz = vs_shfl_down(cur);
+      if (lane == 31 && (meta & nb_bit(5))) {
+        if (j > j0) vz = edge[(par ^ 1) * nwarp + warp + 1];
+        else vz = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + 1);
+      }
       V3<R> FX{}, MX{}, BX{}, FY{}, MY{}, BY{}, FZ{}, MZ{}, BZ{};
       if (meta & M_FILLED) {
         const AFrame<R> f = a_frame(d, cur);
@@ -778,6 +801,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
         if (meta & nb_bit(1)) bond_eval<0>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vx, dT, FX, MX, BX);
         if (meta & nb_bit(3)) bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nxt, dT, FY, MY, BY);
       }
+      if (lane == 0 && warp > 0 && act && j + 1 < j1) edge[par * nwarp + warp] = nxt;
       Rec6<R>* zr = zrec + (size_t)par * nzb;
       if (act) zr[k] = rec6(FZ, BZ);
       // K4's slot order -x, +x, -y, +y | -z, +z: the first four before the barrier
@@ -818,7 +842,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
 }
 
 template <class R> size_t fused_smem(int ty, int nzb) {
-  return sizeof(Rec6<R>) * ((size_t)ty * nzb + 2 * (size_t)nzb);
+  return sizeof(Rec6<R>) * ((size_t)ty * nzb + 2 * (size_t)nzb) + 2 * (size_t)(nzb / 32) * sizeof(VS<R>);
 }
 
 // ------------------------------------------------------------------ fused step, TMA-staged rows
