@@ -231,14 +231,12 @@ __device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
   if constexpr (AX == 0) r.x += l;
   else if constexpr (AX == 1) r.y += l;
   else r.z += l;
-#ifndef VX_EXP_NODAMP
   const V3<R> dV = Vb - Va;
   const V3<R> rw = cross(r, wa + wb);
   const V3<R> dw = wb - wa;
   Fa = Fa + c.ct2 * dV + c.ct4 * rw;
   Ma = Ma + c.cr2 * dw;
   Mbw = Mbw - c.cr2 * dw;
-#endif
 }
 
 // fp32 bond: the same operations in the same order as the generic bond_eval,
@@ -704,6 +702,10 @@ template <class R> struct FusedArgs {
   int nplanes;      // planes in the local box
 };
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // Thread k's +z neighbour is thread k+1's own voxel: a warp shuffle of its
 // registers; lane 31 takes it from the next warp's lane 0 through shared
 // memory (written before the previous row's barrier).
@@ -789,6 +791,14 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
         nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
       VS<R> vx;
       if (meta & nb_bit(1)) vx = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + sx);
+      // the +x row two rows ahead (first touch: HBM) into L2
+      if (act && j + 2 < j1 && i + 1 < a.nplanes) {
+        const uint32_t f = id + sx + 2 * nz;
+        prefetch_l2(d.pos + f);
+        prefetch_l2(d.quat + f);
+        prefetch_l2(d.mom + f);
+        prefetch_l2(d.ang + f);
+      }
       VS<R> vz = vs_shfl_down(cur);
       if (lane == 31 && (meta & nb_bit(5))) {
         if (j > j0) vz = edge[(par ^ 1) * nwarp + warp + 1];
