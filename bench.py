@@ -41,10 +41,11 @@ ALG_BYTES = {
     32: {"bonds": 56 + 108, "integrate": 108 + 56 + 56, "fused": 56 + 56},
     64: {"bonds": 112 + 216, "integrate": 216 + 112 + 112, "fused": 112 + 112},
 }
-# Issue side of the fused kernel, counted by ncu on C5 fp32 (profiles/r03_fused.md):
-# warp-instructions per voxel-step (smsp__thread_inst_executed / 32) and FP32
-# lane-operations (FADD + FMUL + FFMA thread-instructions) per voxel-step.
-FUSED_COUNTS = {32: {"warp_inst": 922.8 / 32, "fp32_ops": 550.3}}
+# Issue side of the fused kernel, counted by ncu on C5 fp32 (profiles/r06_fused.md):
+# issue slots per voxel-step (smsp__inst_executed / voxels), FP32 lane-operations
+# (scalar FADD/FMUL/FFMA thread-instructions + 2 x the packed FADD2/FMUL2/FFMA2
+# ones) and FLOP (an FMA lane-op = 2) per voxel-step.
+FUSED_COUNTS = {32: {"warp_inst": 889430790 / 33554432, "fp32_ops": 547.1, "flop": 841.6}}
 
 
 def alu_roof(prec, ms, voxels, clocks):
@@ -59,11 +60,12 @@ def alu_roof(prec, ms, voxels, clocks):
     mhz = (clocks or {}).get("sm_mhz") or 1965.0
     peak = 4 * 148 * mhz * 1e6 / 1e9                           # G warp-inst / s
     achieved = c["warp_inst"] * voxels / (ms / 1e3) / 1e9
-    fp_peak = 128 * 148 * mhz * 1e6 / 1e12                     # T lane-ops / s
-    fp = c["fp32_ops"] * voxels / (ms / 1e3) / 1e12
+    fp_peak = 2 * 128 * 148 * mhz * 1e6 / 1e12                 # TFLOP/s (FMA = 2)
+    fp = c["flop"] * voxels / (ms / 1e3) / 1e12
     return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
             "frac": achieved / peak, "warp_inst_per_voxel": c["warp_inst"],
-            "fp32": {"achieved": fp, "peak": fp_peak, "unit": "Tlane-op/s", "frac": fp / fp_peak},
+            "fp32": {"achieved": fp, "peak": fp_peak, "unit": "TFLOP/s", "frac": fp / fp_peak,
+                     "flop_per_voxel": c["flop"], "lane_ops_per_voxel": c["fp32_ops"]},
             "peak_note": f"4 issue/clk/SM x 148 SMs x {mhz:.0f} MHz; FP32 128 lanes/SM"}
 
 

@@ -503,7 +503,8 @@ __device__ __forceinline__ float integrate_store_f32(const Dev<float>& d, uint32
 // damping (R12), contacts, floor + friction (R14, R15),
 // integration (Eq. 27-30); writes the new state of `id` to the out arrays.
 template <class R, bool COLLIDE>
-__device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, const VS<R>& s, uint32_t meta,
+__device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, uint32_t kz, const VS<R>& s,
+                                          uint32_t meta,
                                           V3<R> F, V3<R> M, typename VT<R>::R4* __restrict__ opos,
                                           typename VT<R>::R4* __restrict__ oquat,
                                           typename VT<R>::R4* __restrict__ omom,
@@ -546,7 +547,6 @@ __device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, const VS
   bool zero_lat = false;
   if (d.floor_on) {                                   // P:260-274, R14, R15
     const R dT = (R)d.clk->dT;
-    const uint32_t kz = id % d.nz;
     // penetration r_v - (D_z - z_floor), r_v = (l/2)(1 + alpha dT)
     const R base = (R)(d.zbase_d + d.l_d * (double)kz);
     const R pen = d.half_l * mc.alpha * dT - p.z - base;
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(256) k_integrate(Dev<R> d, uint32_t beg, uint3
         }
       }
       s.q = d.quat[id];
-      vmax = finish_voxel<R, COLLIDE>(d, id, s, meta, F, M, d.pos, d.quat, d.mom, d.ang,
+      vmax = finish_voxel<R, COLLIDE>(d, id, id % d.nz, s, meta, F, M, d.pos, d.quat, d.mom, d.ang,
                                       ext_of_local);
     }
   }
@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
           slot_minus(F, M, z);
         }
         if (meta & nb_bit(5)) slot_plus(F, M, FZ, MZ);
-        const R v = finish_voxel<R, COLLIDE>(d, id, cur, meta, F, M, a.opos, a.oquat, a.omom,
+        const R v = finish_voxel<R, COLLIDE>(d, id, k, cur, meta, F, M, a.opos, a.oquat, a.omom,
                                              a.oang, a.ext_of_local);
         vmax = fmax(vmax, v);
       } else if (meta & M_FILLED) {   // fixed: copied through unchanged
@@ -1050,7 +1050,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R
             slot_minus(F, M, z);
           }
           if (meta & nb_bit(5)) slot_plus(F, M, FZ, MZ);
-          const R v = finish_voxel<R, COLLIDE>(d, id, cur, meta, F, M, a.opos, a.oquat, a.omom,
+          const R v = finish_voxel<R, COLLIDE>(d, id, k, cur, meta, F, M, a.opos, a.oquat, a.omom,
                                                a.oang, a.ext_of_local);
           vmax = fmax(vmax, v);
         } else if (meta & M_FILLED) {   // fixed: copied through unchanged
