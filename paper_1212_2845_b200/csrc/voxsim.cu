@@ -162,6 +162,8 @@ struct vx_lattice {
   bool tma_ok = false;                    // TMA-staged fused variant (VX_FUSED_TMA=1; measured slower)
   int fused_ty = 8;                       // rows per fused block (VX_FUSED_TY overrides)
   int fused_waves = 4;                    // block waves per fused launch (VX_FUSED_WAVES)
+  int fused_tune = 1;                     // time candidate segment lengths once (VX_FUSED_TUNE)
+  std::map<long long, int> sx_tuned;      // planes per block segment chosen per launch range
   int batch_stride = 0;                   // planes per batched scene (vx_set_batch)
 
   bool fused() const { return engine == VX_ENGINE_FUSED; }
@@ -540,10 +542,58 @@ template <class R> void launch_integrate(vx_lattice* h, const Slab& s, const Dev
     k_integrate<R, false><<<grid_of(end - beg), 256, 0, h->stream>>>(d, beg, end, s.ext_of_local.as<uint32_t>());
 }
 
+inline long long fused_key(const Slab& s, int x_begin, int x_end) {
+  return ((long long)s.x0 << 40) | ((long long)x_begin << 20) | (long long)x_end;
+}
+
+template <class R>
+vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int x_end, int sx_force = 0);
+
+// Launch-geometry tuning of the fused pass (once per launch range, outside any
+// graph): the step time depends on how the planes split into block segments
+// (the -x halo costs 1/SX of the +x bonds; the block count sets the wave
+// quantisation over 148 SMs x 2 resident blocks) in a way no closed rule
+// captured (profiles/r07_tuning.md).  Each candidate recomputes S_{n+1} from
+// S_n into the spare copy -- the arithmetic per voxel is the same for every
+// segment length, so the state the real step then writes is unchanged.
+template <class R> vx_status tune_fused(vx_lattice* h) {
+  if (!h->fused() || h->fused_tune == 0 || !h->sx_tuned.empty()) return VX_OK;
+  const bool split = h->emulated || h->nccl();
+  const bool col = h->collide();
+  for (const Slab& s : h->slabs) {
+    const int b = split ? s.x0 + 1 : s.x0, e = split ? s.x1 - 1 : s.x1;
+    const int planes = e - b;
+    if (planes < 8 || (long long)planes * h->plane < (1LL << 20)) continue;   // launch-bound: keep default
+    cudaEvent_t e0, e1;
+    VX_CUDA(cudaEventCreate(&e0));
+    VX_CUDA(cudaEventCreate(&e1));
+    float best = 1e30f;
+    int best_sx = 0;
+    static const int cand[] = {3, 4, 5, 6, 7, 8, 10, 12, 14, 16, 20, 24, 32};
+    for (int sx : cand) {
+      if (sx > planes) break;
+      VX_TRY(launch_fused<R>(h, s, col, b, e, sx));   // warm
+      VX_CUDA(cudaEventRecord(e0, h->stream));
+      for (int r = 0; r < 3; ++r) VX_TRY(launch_fused<R>(h, s, col, b, e, sx));
+      VX_CUDA(cudaEventRecord(e1, h->stream));
+      VX_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      VX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      if (ms < best) { best = ms; best_sx = sx; }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (best_sx) h->sx_tuned[fused_key(s, b, e)] = best_sx;
+  }
+  if (h->sx_tuned.empty()) h->sx_tuned[-1] = 0;   // nothing to tune: do not retry
+  h->clear_graphs();
+  return VX_OK;
+}
+
 // Fused single pass over a slab's owned planes: S_n (current copy) -> S_{n+1}
 // (other copy).  Block = one thread per z (nz <= 256) x TY rows x SX planes.
 template <class R>
-vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int x_end) {
+vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int x_end, int sx_force) {
   if (x_end <= x_begin) return VX_OK;
   const Dev<R> d = make_dev<R>(h, s);
   FusedArgs<R> a;
@@ -568,6 +618,13 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
   const int target = 148 * 2 * h->fused_waves;   // blocks: waves at 2 resident blocks per SM
   const int nseg = std::max(1, std::min(planes, (target + a.ntiles_y - 1) / a.ntiles_y));
   a.sx = (planes + nseg - 1) / nseg;
+  // planes per block segment: forced (tuning), tuned for this range, or the default
+  if (sx_force > 0) {
+    a.sx = std::min(sx_force, planes);
+  } else {
+    auto it = h->sx_tuned.find(fused_key(s, x_begin, x_end));
+    if (it != h->sx_tuned.end()) a.sx = std::min(it->second, planes);
+  }
   const int segs = (planes + a.sx - 1) / a.sx;
   const int pi = sizeof(R) == 4 ? 0 : 1;
   if (!h->fused_smem_set[pi]) {
@@ -757,6 +814,7 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
 }
 
 template <class R> vx_status run_steps(vx_lattice* h, long long n) {
+  VX_TRY(tune_fused<R>(h));
   if (h->instr) {
     const size_t need = (size_t)n * 4;
     while (h->events.size() < need) {
@@ -930,6 +988,7 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   if (const char* e = std::getenv("VX_FUSED_TMA")) h->tma_ok = std::atoi(e) != 0;
   if (const char* e = std::getenv("VX_FUSED_TY")) h->fused_ty = std::max(1, std::min(64, std::atoi(e)));
   if (const char* e = std::getenv("VX_FUSED_WAVES")) h->fused_waves = std::max(1, std::min(64, std::atoi(e)));
+  if (const char* e = std::getenv("VX_FUSED_TUNE")) h->fused_tune = std::atoi(e);
   h->cells.assign(desc->cells, desc->cells + cells);
   h->plane = (uint32_t)((long long)h->ny * h->nz);
   h->nbox = (long long)h->nx * h->plane;
