@@ -190,10 +190,7 @@ struct vx_lattice {
   int fused_launches() const {
     if (!(emulated || nccl())) return (int)slabs.size();
     int k = 0;
-    for (const auto& s : slabs) {
-      const int w = s.x1 - s.x0;
-      k += w >= 3 ? 3 : w;
-    }
+    for (const auto& s : slabs) k += (s.x1 - s.x0) >= 3 ? 2 : 1;   // interior + boundary planes
     return k;
   }
   // clock + (surface pack and contact per slab + broadphase when colliding)
@@ -547,7 +544,8 @@ inline long long fused_key(const Slab& s, int x_begin, int x_end) {
 }
 
 template <class R>
-vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int x_end, int sx_force = 0);
+vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int x_end, int sx_force = 0,
+                       cudaStream_t st = nullptr, int x_begin2 = 0, int x_end2 = 0, int ty_force = 0);
 
 // Launch-geometry tuning of the fused pass (once per launch range, outside any
 // graph): the step time depends on how the planes split into block segments
@@ -593,8 +591,10 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
 // Fused single pass over a slab's owned planes: S_n (current copy) -> S_{n+1}
 // (other copy).  Block = one thread per z (nz <= 256) x TY rows x SX planes.
 template <class R>
-vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int x_end, int sx_force) {
+vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int x_end, int sx_force,
+                       cudaStream_t st, int x_begin2, int x_end2, int ty_force) {
   if (x_end <= x_begin) return VX_OK;
+  if (!st) st = h->stream;
   const Dev<R> d = make_dev<R>(h, s);
   FusedArgs<R> a;
   a.opos = s.out(0).as<typename VT<R>::R4>();
@@ -609,7 +609,7 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
   // TMA-staged rows need 16-byte aligned rows of every array (nz even); the
   // rows per block are the most that keep two blocks per SM in shared memory.
   const bool tma = h->tma_ok && (h->nz % 2 == 0);
-  int ty = std::min(h->fused_ty, h->ny);
+  int ty = std::min(ty_force > 0 ? ty_force : h->fused_ty, h->ny);
   if (tma)
     while (ty > 1 && fused_tma_smem<R>(ty, threads) > 110 * 1024) --ty;
   a.ty = ty;
@@ -639,17 +639,35 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
     }
     h->fused_smem_set[pi] = true;
   }
-  const unsigned grid = (unsigned)(a.ntiles_y * segs);
+  a.nblk0 = a.ntiles_y * segs;
+  a.p0b = a.p1b = 0;
+  int segs2 = 0;
+  if (x_end2 > x_begin2) {   // second range, same segment length and rows per block
+    a.p0b = x_begin2 - s.xl0;
+    a.p1b = x_end2 - s.xl0;
+    segs2 = (a.p1b - a.p0b + a.sx - 1) / a.sx;
+  }
+  const unsigned grid = (unsigned)(a.ntiles_y * (segs + segs2));
   if (tma) {
     const size_t smem = fused_tma_smem<R>(a.ty, threads);
-    if (col) k_step_fused_tma<R, true><<<grid, threads, smem, h->stream>>>(d, a);
-    else k_step_fused_tma<R, false><<<grid, threads, smem, h->stream>>>(d, a);
+    if (col) k_step_fused_tma<R, true><<<grid, threads, smem, st>>>(d, a);
+    else k_step_fused_tma<R, false><<<grid, threads, smem, st>>>(d, a);
   } else {
     const size_t smem = fused_smem<R>(a.ty, threads);
-    if (col) k_step_fused<R, true><<<grid, threads, smem, h->stream>>>(d, a);
-    else k_step_fused<R, false><<<grid, threads, smem, h->stream>>>(d, a);
+    if (col) k_step_fused<R, true><<<grid, threads, smem, st>>>(d, a);
+    else k_step_fused<R, false><<<grid, threads, smem, st>>>(d, a);
   }
   return VX_OK;
+}
+
+// A slab's first and last owned planes (they read the ghost planes) in one
+// launch: one plane per segment, TY chosen for about one wave of blocks.
+template <class R> vx_status launch_boundary(vx_lattice* h, const Slab& s, bool col, cudaStream_t st) {
+  const int w = s.x1 - s.x0;
+  const int nb = w >= 2 ? 2 : 1;
+  const int ty = std::max(1, std::min(h->fused_ty, (h->ny * nb + 295) / 296));
+  if (w <= 2) return launch_fused<R>(h, s, col, s.x0, s.x1, 1, st, 0, 0, ty);
+  return launch_fused<R>(h, s, col, s.x0, s.x0 + 1, 1, st, s.x1 - 1, s.x1, ty);
 }
 
 // The four SoA state arrays of a slab, with element sizes.
@@ -763,24 +781,24 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
   if (h->fused()) {
     if (h->nccl()) {
       // ghost planes of S_n on the comm stream, overlapped with the interior
-      // planes [x0+1, x1-1), which read no ghost plane; then the two boundary planes
+      // planes [x0+1, x1-1) (they read no ghost plane) on the main stream; the
+      // two boundary planes follow the exchange on the comm stream, concurrently
+      // with the interior pass
       const Slab& s = h->slabs[0];
       VX_CUDA(cudaEventRecord(h->ev_k4, h->stream));
       VX_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_k4, 0));
       VX_TRY(halo_nccl(h));
-      VX_CUDA(cudaEventRecord(h->ev_halo, h->comm_stream));
       if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
       VX_TRY(launch_fused<R>(h, s, col, s.x0 + 1, s.x1 - 1));
+      VX_TRY(launch_boundary<R>(h, s, col, h->comm_stream));
+      VX_CUDA(cudaEventRecord(h->ev_halo, h->comm_stream));
       VX_CUDA(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
-      VX_TRY(launch_fused<R>(h, s, col, s.x0, std::min(s.x0 + 1, s.x1)));
-      VX_TRY(launch_fused<R>(h, s, col, std::max(s.x1 - 1, s.x0 + 1), s.x1));
     } else {
       if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
       for (const Slab& s : h->slabs) {
         if (h->emulated) {   // the launch split of the NCCL ranks (ghosts already copied)
           VX_TRY(launch_fused<R>(h, s, col, s.x0 + 1, s.x1 - 1));
-          VX_TRY(launch_fused<R>(h, s, col, s.x0, std::min(s.x0 + 1, s.x1)));
-          VX_TRY(launch_fused<R>(h, s, col, std::max(s.x1 - 1, s.x0 + 1), s.x1));
+          VX_TRY(launch_boundary<R>(h, s, col, h->stream));
         } else {
           VX_TRY(launch_fused<R>(h, s, col, s.x0, s.x1));
         }

@@ -100,6 +100,41 @@ template <class R> __device__ __forceinline__ R comp(V3<R> a, int i) {
   return i == 0 ? a.x : (i == 1 ? a.y : a.z);
 }
 
+// ---------------------------------------------------------------- explicit rounding
+// Each helper rounds once, as written: the compiler may not fuse a product
+// into a later sum (FMA contraction).  The frame and bond arithmetic is
+// written with them, so every inlined copy -- a halo recomputation or a row of
+// the fused sweep, K3 -- gives bit-identical results whatever code surrounds
+// it (slab-count and launch-geometry invariance rest on this).
+__device__ __forceinline__ float xmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float xadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float xsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float xfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double xfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+template <class R> __device__ __forceinline__ V3<R> xadd3(V3<R> a, V3<R> b) {
+  return {xadd(a.x, b.x), xadd(a.y, b.y), xadd(a.z, b.z)};
+}
+template <class R> __device__ __forceinline__ V3<R> xsub3(V3<R> a, V3<R> b) {
+  return {xsub(a.x, b.x), xsub(a.y, b.y), xsub(a.z, b.z)};
+}
+template <class R> __device__ __forceinline__ V3<R> xscale3(R s, V3<R> a) {
+  return {xmul(s, a.x), xmul(s, a.y), xmul(s, a.z)};
+}
+template <class R> __device__ __forceinline__ V3<R> xfma3(R s, V3<R> a, V3<R> c) {   // s a + c
+  return {xfma(s, a.x, c.x), xfma(s, a.y, c.y), xfma(s, a.z, c.z)};
+}
+template <class R> __device__ __forceinline__ V3<R> xcross(V3<R> a, V3<R> b) {
+  return {xfma(a.y, b.z, xmul(-a.z, b.y)), xfma(a.z, b.x, xmul(-a.x, b.z)),
+          xfma(a.x, b.y, xmul(-a.y, b.x))};
+}
+// a x + b y + c z, left to right
+template <class R> __device__ __forceinline__ R xdot3(R a, R x, R b, R y, R c, R z) {
+  return xfma(c, z, xfma(b, y, xmul(a, x)));
+}
+
 // Rotation matrix of a unit quaternion, split as R = I + Dm with the
 // diagonal of Dm formed without cancellation (-2(y^2+z^2) ...).
 template <class R> struct Rot {
@@ -109,29 +144,29 @@ template <class R> struct Rot {
 template <class R> __device__ __forceinline__ Rot<R> rotation(R w, R x, R y, R z) {
   Rot<R> r;
   const R two = R(2);
-  r.dd[0] = -two * (y * y + z * z);
-  r.dd[1] = -two * (x * x + z * z);
-  r.dd[2] = -two * (x * x + y * y);
-  r.m[0][0] = R(1) + r.dd[0];
-  r.m[1][1] = R(1) + r.dd[1];
-  r.m[2][2] = R(1) + r.dd[2];
-  r.m[0][1] = two * (x * y - w * z);
-  r.m[0][2] = two * (x * z + w * y);
-  r.m[1][0] = two * (x * y + w * z);
-  r.m[1][2] = two * (y * z - w * x);
-  r.m[2][0] = two * (x * z - w * y);
-  r.m[2][1] = two * (y * z + w * x);
+  r.dd[0] = xmul(-two, xfma(z, z, xmul(y, y)));
+  r.dd[1] = xmul(-two, xfma(z, z, xmul(x, x)));
+  r.dd[2] = xmul(-two, xfma(y, y, xmul(x, x)));
+  r.m[0][0] = xadd(R(1), r.dd[0]);
+  r.m[1][1] = xadd(R(1), r.dd[1]);
+  r.m[2][2] = xadd(R(1), r.dd[2]);
+  r.m[0][1] = xmul(two, xfma(-w, z, xmul(x, y)));
+  r.m[0][2] = xmul(two, xfma(w, y, xmul(x, z)));
+  r.m[1][0] = xmul(two, xfma(w, z, xmul(x, y)));
+  r.m[1][2] = xmul(two, xfma(-w, x, xmul(y, z)));
+  r.m[2][0] = xmul(two, xfma(-w, y, xmul(x, z)));
+  r.m[2][1] = xmul(two, xfma(w, x, xmul(y, z)));
   return r;
 }
 template <class R> __device__ __forceinline__ V3<R> mul(const Rot<R>& r, V3<R> a) {
-  return {r.m[0][0] * a.x + r.m[0][1] * a.y + r.m[0][2] * a.z,
-          r.m[1][0] * a.x + r.m[1][1] * a.y + r.m[1][2] * a.z,
-          r.m[2][0] * a.x + r.m[2][1] * a.y + r.m[2][2] * a.z};
+  return {xdot3(r.m[0][0], a.x, r.m[0][1], a.y, r.m[0][2], a.z),
+          xdot3(r.m[1][0], a.x, r.m[1][1], a.y, r.m[1][2], a.z),
+          xdot3(r.m[2][0], a.x, r.m[2][1], a.y, r.m[2][2], a.z)};
 }
 template <class R> __device__ __forceinline__ V3<R> mulT(const Rot<R>& r, V3<R> a) {
-  return {r.m[0][0] * a.x + r.m[1][0] * a.y + r.m[2][0] * a.z,
-          r.m[0][1] * a.x + r.m[1][1] * a.y + r.m[2][1] * a.z,
-          r.m[0][2] * a.x + r.m[1][2] * a.y + r.m[2][2] * a.z};
+  return {xdot3(r.m[0][0], a.x, r.m[1][0], a.y, r.m[2][0], a.z),
+          xdot3(r.m[0][1], a.x, r.m[1][1], a.y, r.m[2][1], a.z),
+          xdot3(r.m[0][2], a.x, r.m[1][2], a.y, r.m[2][2], a.z)};
 }
 
 // ---------------------------------------------------------------- fp32 pairs
@@ -201,26 +236,26 @@ __device__ __forceinline__ RotP rotation_p(float x, float y, float z, float w) {
   const f2_t r2 = mul2(fma2(nyx, bc2(w), xzyz), bc2(2.f));
   r.dd0 = f2lo(t0);
   r.dd1 = f2hi(t1);
-  r.dd2 = -2.f * (x * x + y * y);
+  r.dd2 = xmul(-2.f, xfma(y, y, xmul(x, x)));
   r.c0 = add2(t0, f2pk(1.f, 0.f));
   r.c1 = add2(t1, f2pk(0.f, 1.f));
   r.pax = f2pk(-x, x);
   r.paz = f2pk(z, -z);
   r.m20 = f2lo(r2);
   r.m21 = f2hi(r2);
-  r.m22 = 1.f + r.dd2;
+  r.m22 = xadd(1.f, r.dd2);
   return r;
 }
 // R a = a.x c0 + a.y c1 + a.z c2 (x, y packed)
 __device__ __forceinline__ V3<float> mul(const RotP& r, V3<float> a) {
   const f2_t xy = fma2(r.c2, bc2(a.z), fma2(r.c1, bc2(a.y), mul2(r.c0, bc2(a.x))));
-  return {f2lo(xy), f2hi(xy), r.m20 * a.x + r.m21 * a.y + r.m22 * a.z};
+  return {f2lo(xy), f2hi(xy), xdot3(r.m20, a.x, r.m21, a.y, r.m22, a.z)};
 }
 // R^T a: one dot product per column
 __device__ __forceinline__ V3<float> mulT(const RotP& r, V3<float> a) {
-  return {f2lo(r.c0) * a.x + f2hi(r.c0) * a.y + r.m20 * a.z,
-          f2lo(r.c1) * a.x + f2hi(r.c1) * a.y + r.m21 * a.z,
-          f2lo(r.c2) * a.x + f2hi(r.c2) * a.y + r.m22 * a.z};
+  return {xdot3(f2lo(r.c0), a.x, f2hi(r.c0), a.y, r.m20, a.z),
+          xdot3(f2lo(r.c1), a.x, f2hi(r.c1), a.y, r.m21, a.z),
+          xdot3(f2lo(r.c2), a.x, f2hi(r.c2), a.y, r.m22, a.z)};
 }
 
 // Cyclic permutation Pi of reading R5: world -> bond frame of axis AX.

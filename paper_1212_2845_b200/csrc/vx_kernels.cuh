@@ -151,13 +151,13 @@ template <class R> struct SeriesCut;
 template <> struct SeriesCut<float> { static constexpr float s2 = 0.125f * 0.125f; };
 template <> struct SeriesCut<double> { static constexpr double s2 = 0.002 * 0.002; };
 template <class R> __device__ __forceinline__ R rotvec_scale(R w, R x, R y, R z) {
-  const R s2 = x * x + y * y + z * z;
+  const R s2 = xdot3(x, x, y, y, z, z);
   if (s2 < SeriesCut<R>::s2) {
-    return R(2) + s2 * (R(1) / R(3) + s2 * (R(3) / R(20) + s2 * (R(5) / R(56) +
-                                                          s2 * (R(35) / R(576)))));
+    return xfma(s2, xfma(s2, xfma(s2, xfma(s2, R(35) / R(576), R(5) / R(56)), R(3) / R(20)),
+                         R(1) / R(3)), R(2));
   }
   const R s = vx_sqrt(s2);
-  return R(2) * vx_atan2(s, w) / s;
+  return xmul(R(2), vx_atan2(s, w)) / s;
 }
 
 // Voxel a (negative side, R4) and b = a + e_AX.  Loads in the frame of a
@@ -194,29 +194,33 @@ __device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
 
   // relative position in a's frame, cancellation-free:
   //   R^T r - l e = l (R^T e - e) + R^T (u_b - u_a)
-  const V3<R> du = mk(pb.x - ua.x, pb.y - ua.y, pb.z - ua.z);
+  const V3<R> du = xsub3(mk(pb.x, pb.y, pb.z), ua);
   V3<R> t;  // R^T e_AX - e_AX = row AX of (R - I)
   if constexpr (AX == 0) t = mk(Ra.dd[0], Ra.m[0][1], Ra.m[0][2]);
   else if constexpr (AX == 1) t = mk(Ra.m[1][0], Ra.dd[1], Ra.m[1][2]);
   else t = mk(Ra.m[2][0], Ra.m[2][1], Ra.dd[2]);
-  const V3<R> dv = to_bond<AX>(l * t + mulT(Ra, du));
+  const V3<R> dv = to_bond<AX>(xfma3(l, t, mulT(Ra, du)));
 
-  // relative rotation theta = rotvec(q_a* q_b), w >= 0 (R6, R7)
-  R qw = qa.w * qb.w + qa.x * qb.x + qa.y * qb.y + qa.z * qb.z;
-  R qx = qa.w * qb.x - qa.x * qb.w - qa.y * qb.z + qa.z * qb.y;
-  R qy = qa.w * qb.y + qa.x * qb.z - qa.y * qb.w - qa.z * qb.x;
-  R qz = qa.w * qb.z - qa.x * qb.y + qa.y * qb.x - qa.z * qb.w;
+  // relative rotation theta = rotvec(q_a* q_b), w >= 0 (R6, R7); each
+  // component summed a_w b + a_x b + a_y b + a_z b, left to right
+  const R qw = xfma(qa.z, qb.z, xfma(qa.y, qb.y, xfma(qa.x, qb.x, xmul(qa.w, qb.w))));
+  const R qx = xfma(qa.z, qb.y, xfma(-qa.y, qb.z, xfma(-qa.x, qb.w, xmul(qa.w, qb.x))));
+  const R qy = xfma(-qa.z, qb.x, xfma(-qa.y, qb.w, xfma(qa.x, qb.z, xmul(qa.w, qb.y))));
+  const R qz = xfma(-qa.z, qb.w, xfma(qa.y, qb.x, xfma(-qa.x, qb.y, xmul(qa.w, qb.z))));
   // w < 0: theta of -q_rel (the same rotation); the sign folds into the scale
-  const R sg = qw < R(0) ? R(-1) : R(1);
-  const V3<R> th = to_bond<AX>((sg * rotvec_scale(fabs(qw), qx, qy, qz)) * mk(qx, qy, qz));
+  const R kth = (qw < R(0) ? R(-1) : R(1)) * rotvec_scale(fabs(qw), qx, qy, qz);
+  const V3<R> th = to_bond<AX>(xscale3(kth, mk(qx, qy, qz)));
 
   // Eq. 40: X2 = d_x - L_T with L_T = l (1 + alpha_mean dT)
-  const R X2 = dv.x - l * c.alpha_mean * dT;
+  const R X2 = xsub(dv.x, xmul(xmul(l, c.alpha_mean), dT));
   const R Y2 = dv.y, Z2 = dv.z;
-  const V3<R> fa = mk(c.a1 * X2, c.b1 * Y2 - c.b2 * th.z, c.b1 * Z2 + c.b2 * th.y);
-  const V3<R> ma = mk(c.a2 * th.x, -c.b2 * Z2 - c.b3 * th.y, c.b2 * Y2 - c.b3 * th.z);
-  const V3<R> mbl = mk(-c.a2 * th.x, -c.b2 * Z2 - R(2) * c.b3 * th.y,
-                       c.b2 * Y2 - R(2) * c.b3 * th.z);
+  const R b3x2 = R(2) * c.b3;
+  const V3<R> fa = mk(xmul(c.a1, X2), xfma(-c.b2, th.z, xmul(c.b1, Y2)),
+                      xfma(c.b2, th.y, xmul(c.b1, Z2)));
+  const V3<R> ma = mk(xmul(c.a2, th.x), xfma(-c.b3, th.y, xmul(-c.b2, Z2)),
+                      xfma(-c.b3, th.z, xmul(c.b2, Y2)));
+  const V3<R> mbl = mk(xmul(-c.a2, th.x), xfma(-b3x2, th.y, xmul(-c.b2, Z2)),
+                       xfma(-b3x2, th.z, xmul(c.b2, Y2)));
   Fa = mul(Ra, to_world<AX>(fa));
   Ma = mul(Ra, to_world<AX>(ma));
   Mbw = mul(Ra, to_world<AX>(mbl));
@@ -225,18 +229,18 @@ __device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
   //   V_r = (V_b - V_avg) + (r/2) x w_avg = (V_b - V_a)/2 + (r x (w_a + w_b))/4
   //   w_r = w_b - w_avg = (w_b - w_a)/2
   // and c_t/2, c_t/4, c_r/2 come from the pair table (exact power-of-2 scalings).
-  const V3<R> Vb = c.inv_m_b * mk(b.mo.x, b.mo.y, b.mo.z);
-  const V3<R> wb = c.inv_I_b * mk(b.an.x, b.an.y, b.mo.w);
+  const V3<R> Vb = xscale3(c.inv_m_b, mk(b.mo.x, b.mo.y, b.mo.z));
+  const V3<R> wb = xscale3(c.inv_I_b, mk(b.an.x, b.an.y, b.mo.w));
   V3<R> r = du;
-  if constexpr (AX == 0) r.x += l;
-  else if constexpr (AX == 1) r.y += l;
-  else r.z += l;
-  const V3<R> dV = Vb - Va;
-  const V3<R> rw = cross(r, wa + wb);
-  const V3<R> dw = wb - wa;
-  Fa = Fa + c.ct2 * dV + c.ct4 * rw;
-  Ma = Ma + c.cr2 * dw;
-  Mbw = Mbw - c.cr2 * dw;
+  if constexpr (AX == 0) r.x = xadd(r.x, l);
+  else if constexpr (AX == 1) r.y = xadd(r.y, l);
+  else r.z = xadd(r.z, l);
+  const V3<R> dV = xsub3(Vb, Va);
+  const V3<R> rw = xcross(r, xadd3(wa, wb));
+  const V3<R> dw = xsub3(wb, wa);
+  Fa = xfma3(c.ct4, rw, xfma3(c.ct2, dV, Fa));
+  Ma = xfma3(c.cr2, dw, Ma);
+  Mbw = xfma3(-c.cr2, dw, Mbw);
 }
 
 // fp32 bond: the same operations in the same order as the generic bond_eval,
@@ -257,12 +261,12 @@ __device__ __forceinline__ void bond_eval(const Dev<float>& d, const RotP& Ra, c
   const float l = d.l;
 
   const f2_t duxy = sub2(f2pk(pb.x, pb.y), f2pk(ua.x, ua.y));
-  const V3<float> du = mk(f2lo(duxy), f2hi(duxy), pb.z - ua.z);
+  const V3<float> du = mk(f2lo(duxy), f2hi(duxy), xsub(pb.z, ua.z));
   V3<float> t;  // R^T e_AX - e_AX = row AX of (R - I)
   if constexpr (AX == 0) t = mk(Ra.dd0, f2lo(Ra.c1), f2lo(Ra.c2));
   else if constexpr (AX == 1) t = mk(f2hi(Ra.c0), Ra.dd1, f2hi(Ra.c2));
   else t = mk(Ra.m20, Ra.m21, Ra.dd2);
-  const V3<float> dv = to_bond<AX>(l * t + mulT(Ra, du));
+  const V3<float> dv = to_bond<AX>(xfma3(l, t, mulT(Ra, du)));
 
   // q_rel = q_a* q_b, with the swapped pairs (by, bx), (bw, bz) and the
   // per-voxel sign pairs (-ax, ax), (az, -az):
@@ -276,34 +280,37 @@ __device__ __forceinline__ void bond_eval(const Dev<float>& d, const RotP& Ra, c
   const float qx = f2lo(qxy), qy = f2hi(qxy), qz = f2lo(qzw), qw = f2hi(qzw);
   const float kth = (qw < 0.f ? -1.f : 1.f) * rotvec_scale(fabsf(qw), qx, qy, qz);
   const f2_t thxy = mul2(bc2(kth), qxy);
-  const V3<float> th = to_bond<AX>(mk(f2lo(thxy), f2hi(thxy), kth * qz));
+  const V3<float> th = to_bond<AX>(mk(f2lo(thxy), f2hi(thxy), xmul(kth, qz)));
 
-  const float X2 = dv.x - l * c.alpha_mean * dT;
+  const float X2 = xsub(dv.x, xmul(xmul(l, c.alpha_mean), dT));
   const float Y2 = dv.y, Z2 = dv.z;
-  const V3<float> fa = mk(c.a1 * X2, c.b1 * Y2 - c.b2 * th.z, c.b1 * Z2 + c.b2 * th.y);
-  const V3<float> ma = mk(c.a2 * th.x, -c.b2 * Z2 - c.b3 * th.y, c.b2 * Y2 - c.b3 * th.z);
-  const V3<float> mbl = mk(-c.a2 * th.x, -c.b2 * Z2 - 2.f * c.b3 * th.y,
-                           c.b2 * Y2 - 2.f * c.b3 * th.z);
+  const float b3x2 = 2.f * c.b3;
+  const V3<float> fa = mk(xmul(c.a1, X2), xfma(-c.b2, th.z, xmul(c.b1, Y2)),
+                          xfma(c.b2, th.y, xmul(c.b1, Z2)));
+  const V3<float> ma = mk(xmul(c.a2, th.x), xfma(-c.b3, th.y, xmul(-c.b2, Z2)),
+                          xfma(-c.b3, th.z, xmul(c.b2, Y2)));
+  const V3<float> mbl = mk(xmul(-c.a2, th.x), xfma(-b3x2, th.y, xmul(-c.b2, Z2)),
+                           xfma(-b3x2, th.z, xmul(c.b2, Y2)));
   Fa = mul(Ra, to_world<AX>(fa));
   Ma = mul(Ra, to_world<AX>(ma));
   Mbw = mul(Ra, to_world<AX>(mbl));
 
   // Eq. 33-35 (see the generic bond_eval)
   const f2_t Vbxy = mul2(bc2(c.inv_m_b), f2pk(b.mo.x, b.mo.y));
-  const float Vbz = c.inv_m_b * b.mo.z;
+  const float Vbz = xmul(c.inv_m_b, b.mo.z);
   const f2_t wbxy = mul2(bc2(c.inv_I_b), f2pk(b.an.x, b.an.y));
-  const float wbz = c.inv_I_b * b.mo.w;
+  const float wbz = xmul(c.inv_I_b, b.mo.w);
   V3<float> r = du;
-  if constexpr (AX == 0) r.x += l;
-  else if constexpr (AX == 1) r.y += l;
-  else r.z += l;
+  if constexpr (AX == 0) r.x = xadd(r.x, l);
+  else if constexpr (AX == 1) r.y = xadd(r.y, l);
+  else r.z = xadd(r.z, l);
   const f2_t waxy = f2pk(wa.x, wa.y);
   const f2_t dVxy = sub2(Vbxy, f2pk(Va.x, Va.y));
-  const float dVz = Vbz - Va.z;
+  const float dVz = xsub(Vbz, Va.z);
   const f2_t sxy = add2(waxy, wbxy);
-  const V3<float> rw = cross(r, mk(f2lo(sxy), f2hi(sxy), wa.z + wbz));
+  const V3<float> rw = xcross(r, mk(f2lo(sxy), f2hi(sxy), xadd(wa.z, wbz)));
   const f2_t dwxy = sub2(wbxy, waxy);
-  const float dwz = wbz - wa.z;
+  const float dwz = xsub(wbz, wa.z);
   const f2_t Fxy = fma2(bc2(c.ct4), f2pk(rw.x, rw.y), fma2(bc2(c.ct2), dVxy, f2pk(Fa.x, Fa.y)));
   Fa = mk(f2lo(Fxy), f2hi(Fxy), fmaf(c.ct4, rw.z, fmaf(c.ct2, dVz, Fa.z)));
   const f2_t Mxy = fma2(bc2(c.cr2), dwxy, f2pk(Ma.x, Ma.y));
@@ -330,12 +337,12 @@ template <class R> __device__ __forceinline__ AFrame<R> a_frame(const Dev<R>& d,
     f.Ra = rotation_p(a.q.x, a.q.y, a.q.z, a.q.w);
     const f2_t vxy = mul2(bc2(M.inv_m), f2pk(a.mo.x, a.mo.y));
     const f2_t wxy = mul2(bc2(M.inv_I), f2pk(a.an.x, a.an.y));
-    f.Va = mk(f2lo(vxy), f2hi(vxy), M.inv_m * a.mo.z);
-    f.wa = mk(f2lo(wxy), f2hi(wxy), M.inv_I * a.mo.w);
+    f.Va = mk(f2lo(vxy), f2hi(vxy), xmul(M.inv_m, a.mo.z));
+    f.wa = mk(f2lo(wxy), f2hi(wxy), xmul(M.inv_I, a.mo.w));
   } else {
     f.Ra = rotation(a.q.w, a.q.x, a.q.y, a.q.z);
-    f.Va = M.inv_m * mk(a.mo.x, a.mo.y, a.mo.z);
-    f.wa = M.inv_I * mk(a.an.x, a.an.y, a.mo.w);
+    f.Va = xscale3(M.inv_m, mk(a.mo.x, a.mo.y, a.mo.z));
+    f.wa = xscale3(M.inv_I, mk(a.an.x, a.an.y, a.mo.w));
   }
   return f;
 }
@@ -698,6 +705,8 @@ template <class R> struct FusedArgs {
   int ty;           // rows per block
   int sx;           // planes per segment
   int p0, p1;       // local planes to update [p0, p1)
+  int p0b, p1b;     // a second range, for blocks >= nblk0 (a slab's two boundary planes)
+  int nblk0;
   int ntiles_y;
   int nplanes;      // planes in the local box
 };
@@ -737,12 +746,14 @@ __global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a)
 
   const int k = threadIdx.x;
   const bool act = k < (int)d.nz;
-  const int tile = blockIdx.x % a.ntiles_y;
-  const int seg = blockIdx.x / a.ntiles_y;
+  int bid = blockIdx.x, p0 = a.p0, p1 = a.p1;
+  if (bid >= a.nblk0) { bid -= a.nblk0; p0 = a.p0b; p1 = a.p1b; }
+  const int tile = bid % a.ntiles_y;
+  const int seg = bid / a.ntiles_y;
   const int j0 = tile * a.ty;
   const int j1 = min(j0 + a.ty, (int)d.ny);
-  const int i0 = a.p0 + seg * a.sx;
-  const int i1 = min(i0 + a.sx, a.p1);
+  const int i0 = p0 + seg * a.sx;
+  const int i1 = min(i0 + a.sx, p1);
   const uint32_t sx = d.sx, nz = d.nz;
   const int ny = (int)d.ny;
   const R dT = (R)d.clk->dT;
@@ -936,12 +947,14 @@ __global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R
 
   const int k = threadIdx.x;
   const bool act = k < (int)d.nz;
-  const int tile = blockIdx.x % a.ntiles_y;
-  const int seg = blockIdx.x / a.ntiles_y;
+  int bid = blockIdx.x, p0 = a.p0, p1 = a.p1;
+  if (bid >= a.nblk0) { bid -= a.nblk0; p0 = a.p0b; p1 = a.p1b; }
+  const int tile = bid % a.ntiles_y;
+  const int seg = bid / a.ntiles_y;
   const int j0 = tile * a.ty;
   const int j1 = min(j0 + a.ty, (int)d.ny);
-  const int i0 = a.p0 + seg * a.sx;
-  const int i1 = min(i0 + a.sx, a.p1);
+  const int i0 = p0 + seg * a.sx;
+  const int i1 = min(i0 + a.sx, p1);
   const uint32_t sx = d.sx, nz = d.nz;
   const R dT = (R)d.clk->dT;
   R vmax = R(0);
