@@ -732,7 +732,7 @@ template <class R> __device__ __forceinline__ VS<R> vs_shfl_down(const VS<R>& s)
 }
 
 template <class R, bool COLLIDE>
-__global__ void __launch_bounds__(256, 2) k_step_fused(Dev<R> d, FusedArgs<R> a) {
+__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<R> d, FusedArgs<R> a) {
   using R4 = typename VT<R>::R4;
   using R2 = typename VT<R>::R2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
