@@ -12,6 +12,8 @@
 #pragma once
 #include "vx_common.cuh"
 
+#include <type_traits>
+
 namespace vx {
 
 // Device-resident per-lattice scalars (one allocation).
@@ -795,15 +797,19 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
     }
     // One row: voxel (i, j, k) in `cur`; loads row j+1's voxel into `nxt`.  One
     // block barrier: the -z slot (thread k-1's +z bond) goes through zrec[par].
-    auto row = [&](int j, const VS<R>& cur, VS<R>& nxt, int par) {
-      const uint32_t meta = act ? meta_of(cur.p.w) : 0u;
+    // FULL (a warp-uniform compile-time flag): every lane is an active, filled,
+    // non-fixed voxel with all four x/y neighbours -- the interior of a solid;
+    // the per-lane tests of those conditions and their branches drop out.
+    auto row = [&](auto full, int j, const VS<R>& cur, VS<R>& nxt, int par) {
+      constexpr bool FULL = decltype(full)::value;
+      const uint32_t meta = (FULL || act) ? meta_of(cur.p.w) : 0u;
       const uint32_t id = idx(i, j);
-      if (act && (j + 1 < j1 || (meta & nb_bit(3))))
+      if (FULL || (act && (j + 1 < j1 || (meta & nb_bit(3)))))
         nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
       VS<R> vx;
-      if (meta & nb_bit(1)) vx = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + sx);
+      if (FULL || (meta & nb_bit(1))) vx = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + sx);
       // the +x row two rows ahead (first touch: HBM) into L2
-      if (act && j + 2 < j1 && i + 1 < a.nplanes) {
+      if ((FULL || act) && j + 2 < j1 && i + 1 < a.nplanes) {
         const uint32_t f = id + sx + 2 * nz;
         prefetch_l2(d.pos + f);
         prefetch_l2(d.quat + f);
@@ -816,27 +822,29 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
         else vz = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + 1);
       }
       V3<R> FX{}, MX{}, BX{}, FY{}, MY{}, BY{}, FZ{}, MZ{}, BZ{};
-      if (meta & M_FILLED) {
+      if (FULL || (meta & M_FILLED)) {
         const AFrame<R> f = a_frame(d, cur);
         if (meta & nb_bit(5)) bond_eval<2>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vz, dT, FZ, MZ, BZ);
-        if (meta & nb_bit(1)) bond_eval<0>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vx, dT, FX, MX, BX);
-        if (meta & nb_bit(3)) bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nxt, dT, FY, MY, BY);
+        if (FULL || (meta & nb_bit(1)))
+          bond_eval<0>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vx, dT, FX, MX, BX);
+        if (FULL || (meta & nb_bit(3)))
+          bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nxt, dT, FY, MY, BY);
       }
-      if (lane == 0 && warp > 0 && act && j + 1 < j1) edge[par * nwarp + warp] = nxt;
+      if (lane == 0 && warp > 0 && (FULL || act) && j + 1 < j1) edge[par * nwarp + warp] = nxt;
       Rec6<R>* zr = zrec + (size_t)par * nzb;
-      if (act) zr[k] = rec6(FZ, BZ);
+      if (FULL || act) zr[k] = rec6(FZ, BZ);
       // K4's slot order -x, +x, -y, +y | -z, +z: the first four before the barrier
       Rec6<R>& xr = xrec[(size_t)(j - j0) * nzb + k];
       V3<R> F = mk(R(0), R(0), R(0)), M = F;
-      if (meta & nb_bit(0)) { slot_minus(F, M, xr); }
-      if (meta & nb_bit(1)) slot_plus(F, M, FX, MX);
-      if (meta & nb_bit(2)) { slot_minus(F, M, ry); }
-      if (meta & nb_bit(3)) slot_plus(F, M, FY, MY);
-      if (act && (meta & M_FILLED)) xr = rec6(FX, BX);
+      if (FULL || (meta & nb_bit(0))) slot_minus(F, M, xr);
+      if (FULL || (meta & nb_bit(1))) slot_plus(F, M, FX, MX);
+      if (FULL || (meta & nb_bit(2))) slot_minus(F, M, ry);
+      if (FULL || (meta & nb_bit(3))) slot_plus(F, M, FY, MY);
+      if (FULL || (act && (meta & M_FILLED))) xr = rec6(FX, BX);
       ry = rec6(FY, BY);
       __syncthreads();
-      if (!act) return;
-      if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
+      if (!FULL && !act) return;
+      if (FULL || (meta & (M_FILLED | M_FIXED)) == M_FILLED) {
         if (meta & nb_bit(4)) {
           const Rec6<R>& z = zr[k - 1];
           slot_minus(F, M, z);
@@ -854,8 +862,12 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
         st_stream(a.opos + id, cur.p);   // empty cell: meta only
       }
     };
+    constexpr uint32_t kXY = nb_bit(0) | nb_bit(1) | nb_bit(2) | nb_bit(3);
     for (int j = j0; j < j1; ++j) {
-      row(j, va, vb, (j - j0) & 1);
+      const uint32_t m = act ? meta_of(va.p.w) : 0u;
+      const bool full = __all_sync(0xffffffffu, (m & (M_FILLED | M_FIXED | kXY)) == (M_FILLED | kXY));
+      if (full) row(std::true_type{}, j, va, vb, (j - j0) & 1);
+      else row(std::false_type{}, j, va, vb, (j - j0) & 1);
       va = vb;
     }
   }
