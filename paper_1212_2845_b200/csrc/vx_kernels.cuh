@@ -744,6 +744,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
   Rec6<R>* xrec = reinterpret_cast<Rec6<R>*>(smem_raw);
   Rec6<R>* zrec = xrec + (size_t)a.ty * nzb;
   VS<R>* edge = reinterpret_cast<VS<R>*>(zrec + 2 * (size_t)nzb);
+  Rec6<R>* yrec = reinterpret_cast<Rec6<R>*>(edge + 2 * (nzb / 32));   // thread-private -y slot
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = nzb >> 5;
 
   const int k = threadIdx.x;
@@ -782,7 +783,8 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
 
   for (int i = i0; i < i1; ++i) {
     VS<R> va, vb;    // ping-pong: this row's voxel and the next row's
-    Rec6<R> ry{};    // -y slot record of the current row: +y bond of the row below
+    Rec6<R>& ry = yrec[k];   // -y slot record of the current row: +y bond of the row below
+    ry = Rec6<R>{};
     if (act) {
       va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0));
       if (j0 > 0) {   // halo row j0 - 1: its +y bond only
@@ -875,7 +877,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
 }
 
 template <class R> size_t fused_smem(int ty, int nzb) {
-  return sizeof(Rec6<R>) * ((size_t)ty * nzb + 2 * (size_t)nzb) + 2 * (size_t)(nzb / 32) * sizeof(VS<R>);
+  return sizeof(Rec6<R>) * ((size_t)ty * nzb + 3 * (size_t)nzb) + 2 * (size_t)(nzb / 32) * sizeof(VS<R>);
 }
 
 // ------------------------------------------------------------------ fused step, TMA-staged rows
