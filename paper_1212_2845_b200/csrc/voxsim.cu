@@ -163,7 +163,7 @@ struct vx_lattice {
   int fused_ty = 8;                       // rows per fused block (VX_FUSED_TY overrides)
   int fused_waves = 4;                    // block waves per fused launch (VX_FUSED_WAVES)
   int fused_tune = 1;                     // time candidate segment lengths once (VX_FUSED_TUNE)
-  std::map<long long, int> sx_tuned;      // planes per block segment chosen per launch range
+  std::map<long long, std::pair<int, int>> geo_tuned;   // (TY, SX) chosen per launch range
   int batch_stride = 0;                   // planes per batched scene (vx_set_batch)
 
   bool fused() const { return engine == VX_ENGINE_FUSED; }
@@ -548,42 +548,61 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
                        cudaStream_t st = nullptr, int x_begin2 = 0, int x_end2 = 0, int ty_force = 0);
 
 // Launch-geometry tuning of the fused pass (once per launch range, outside any
-// graph): the step time depends on how the planes split into block segments
-// (the -x halo costs 1/SX of the +x bonds; the block count sets the wave
-// quantisation over 148 SMs x 2 resident blocks) in a way no closed rule
-// captured (profiles/r07_tuning.md).  Each candidate recomputes S_{n+1} from
-// S_n into the spare copy -- the arithmetic per voxel is the same for every
-// segment length, so the state the real step then writes is unchanged.
+// graph).  The step time depends on rows per block (TY) and planes per block
+// segment (SX): the -y / -x halos cost 1/TY and 1/SX extra bonds, a block's
+// rows are a serial chain (small lattices want many one-row blocks, TY = SX =
+// 1: C4 22 -> 7 us/step), and the block count sets the wave quantisation over
+// 148 SMs x 2 resident blocks -- in a way no closed rule captured
+// (profiles/r07_tuning.md).  Each candidate recomputes S_{n+1} from S_n into
+// the spare copy; the arithmetic per voxel is the same for every geometry
+// (explicit rounding, tests/test_gpu_geometry.py), so the state the real step
+// then writes is unchanged.  VX_FUSED_TY / VX_FUSED_WAVES fix the geometry.
 template <class R> vx_status tune_fused(vx_lattice* h) {
-  if (!h->fused() || h->fused_tune == 0 || !h->sx_tuned.empty()) return VX_OK;
+  if (!h->fused() || h->fused_tune == 0 || !h->geo_tuned.empty()) return VX_OK;
   const bool split = h->emulated || h->nccl();
   const bool col = h->collide();
+  Clock saved;   // the candidates' motion-budget / divergence atomics must not leak
+  VX_CUDA(cudaMemcpy(&saved, h->clk.p, sizeof saved, cudaMemcpyDeviceToHost));
+  cudaEvent_t e0, e1;
+  VX_CUDA(cudaEventCreate(&e0));
+  VX_CUDA(cudaEventCreate(&e1));
   for (const Slab& s : h->slabs) {
     const int b = split ? s.x0 + 1 : s.x0, e = split ? s.x1 - 1 : s.x1;
     const int planes = e - b;
-    if (planes < 8 || (long long)planes * h->plane < (1LL << 20)) continue;   // launch-bound: keep default
-    cudaEvent_t e0, e1;
-    VX_CUDA(cudaEventCreate(&e0));
-    VX_CUDA(cudaEventCreate(&e1));
+    if (planes < 1) continue;
+    const bool big = (long long)planes * h->plane >= (1LL << 22);
+    static const int ty_big[] = {6, 8}, ty_small[] = {1, 2, 4, 8};
+    static const int sx_big[] = {3, 4, 5, 6, 7, 8, 10, 12, 14, 16, 20, 24, 32};
+    static const int sx_small[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
+    const int* tys = big ? ty_big : ty_small;
+    const int nty = big ? 2 : 4;
+    const int* sxs = big ? sx_big : sx_small;
+    const int nsx = big ? 13 : 10;
+    const int reps = big ? 3 : 8;
     float best = 1e30f;
-    int best_sx = 0;
-    static const int cand[] = {3, 4, 5, 6, 7, 8, 10, 12, 14, 16, 20, 24, 32};
-    for (int sx : cand) {
-      if (sx > planes) break;
-      VX_TRY(launch_fused<R>(h, s, col, b, e, sx));   // warm
-      VX_CUDA(cudaEventRecord(e0, h->stream));
-      for (int r = 0; r < 3; ++r) VX_TRY(launch_fused<R>(h, s, col, b, e, sx));
-      VX_CUDA(cudaEventRecord(e1, h->stream));
-      VX_CUDA(cudaEventSynchronize(e1));
-      float ms = 0;
-      VX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-      if (ms < best) { best = ms; best_sx = sx; }
+    std::pair<int, int> best_g{0, 0};
+    for (int a = 0; a < nty; ++a) {
+      const int ty = tys[a];
+      if (ty > h->ny && ty != tys[0]) break;
+      for (int c = 0; c < nsx; ++c) {
+        const int sx = sxs[c];
+        if (sx > planes && c > 0) break;
+        VX_TRY(launch_fused<R>(h, s, col, b, e, sx, nullptr, 0, 0, ty));   // warm
+        VX_CUDA(cudaEventRecord(e0, h->stream));
+        for (int r = 0; r < reps; ++r) VX_TRY(launch_fused<R>(h, s, col, b, e, sx, nullptr, 0, 0, ty));
+        VX_CUDA(cudaEventRecord(e1, h->stream));
+        VX_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        VX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms < best) { best = ms; best_g = {ty, sx}; }
+      }
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (best_sx) h->sx_tuned[fused_key(s, b, e)] = best_sx;
+    if (best_g.first) h->geo_tuned[fused_key(s, b, e)] = best_g;
   }
-  if (h->sx_tuned.empty()) h->sx_tuned[-1] = 0;   // nothing to tune: do not retry
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  VX_CUDA(cudaMemcpy(h->clk.p, &saved, sizeof saved, cudaMemcpyHostToDevice));
+  if (h->geo_tuned.empty()) h->geo_tuned[-1] = {0, 0};   // nothing to tune: do not retry
   h->clear_graphs();
   return VX_OK;
 }
@@ -609,7 +628,11 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
   // TMA-staged rows need 16-byte aligned rows of every array (nz even); the
   // rows per block are the most that keep two blocks per SM in shared memory.
   const bool tma = h->tma_ok && (h->nz % 2 == 0);
-  int ty = std::min(ty_force > 0 ? ty_force : h->fused_ty, h->ny);
+  // rows per block and planes per segment: forced (tuning, boundary planes),
+  // tuned for this range, or the defaults
+  const auto tuned = h->geo_tuned.find(fused_key(s, x_begin, x_end));
+  const bool have = tuned != h->geo_tuned.end() && tuned->second.first > 0;
+  int ty = std::min(ty_force > 0 ? ty_force : (have ? tuned->second.first : h->fused_ty), h->ny);
   if (tma)
     while (ty > 1 && fused_tma_smem<R>(ty, threads) > 110 * 1024) --ty;
   a.ty = ty;
@@ -618,13 +641,8 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
   const int target = 148 * 2 * h->fused_waves;   // blocks: waves at 2 resident blocks per SM
   const int nseg = std::max(1, std::min(planes, (target + a.ntiles_y - 1) / a.ntiles_y));
   a.sx = (planes + nseg - 1) / nseg;
-  // planes per block segment: forced (tuning), tuned for this range, or the default
-  if (sx_force > 0) {
-    a.sx = std::min(sx_force, planes);
-  } else {
-    auto it = h->sx_tuned.find(fused_key(s, x_begin, x_end));
-    if (it != h->sx_tuned.end()) a.sx = std::min(it->second, planes);
-  }
+  if (sx_force > 0) a.sx = std::min(sx_force, planes);
+  else if (have) a.sx = std::min(tuned->second.second, planes);
   const int segs = (planes + a.sx - 1) / a.sx;
   const int pi = sizeof(R) == 4 ? 0 : 1;
   if (!h->fused_smem_set[pi]) {
@@ -1004,8 +1022,14 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   h->device = desc->device; h->rank = desc->rank; h->nranks = desc->nranks;
   h->emulated = emulated;
   if (const char* e = std::getenv("VX_FUSED_TMA")) h->tma_ok = std::atoi(e) != 0;
-  if (const char* e = std::getenv("VX_FUSED_TY")) h->fused_ty = std::max(1, std::min(64, std::atoi(e)));
-  if (const char* e = std::getenv("VX_FUSED_WAVES")) h->fused_waves = std::max(1, std::min(64, std::atoi(e)));
+  if (const char* e = std::getenv("VX_FUSED_TY")) {
+    h->fused_ty = std::max(1, std::min(64, std::atoi(e)));
+    h->fused_tune = 0;   // an explicit geometry is not tuned away
+  }
+  if (const char* e = std::getenv("VX_FUSED_WAVES")) {
+    h->fused_waves = std::max(1, std::min(64, std::atoi(e)));
+    h->fused_tune = 0;
+  }
   if (const char* e = std::getenv("VX_FUSED_TUNE")) h->fused_tune = std::atoi(e);
   h->cells.assign(desc->cells, desc->cells + cells);
   h->plane = (uint32_t)((long long)h->ny * h->nz);
