@@ -144,6 +144,7 @@ struct vx_lattice {
   std::vector<int> seg;                   // nranks + 1: surface segment of each rank's slab
   DevBuf surf_d, ss, cellh, bcount, bstart, bitems, rowptr, col;
   int H = 0;
+  int bp_grid = 1;                        // CTAs of the cooperative broadphase
   long long cap = 0;
   double cutoff = 0;
   // graphs
@@ -488,6 +489,13 @@ vx_status setup_collision(vx_lattice* h) {
   int H = 1024;
   while (H < 2 * S) H <<= 1;
   h->H = H;
+  {   // cooperative broadphase grid: resident CTAs, no more than the work needs
+    int per_sm = 0, sms = 0;
+    VX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, h->prec == 32 ? (const void*)k_broadphase<float> : (const void*)k_broadphase<double>, 1024, 0));
+    VX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    h->bp_grid = std::max(1, std::min(std::max(1, per_sm) * sms, (std::max(S, H) + 1023) / 1024));
+  }
   const int rows = h->rows_end() - h->rows_begin();
   h->cap = std::max<long long>(1 << 16, 128LL * rows);
   VX_TRY(h->cellh.alloc((size_t)std::max(S, 1) * sizeof(int4)));
@@ -783,9 +791,15 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
                 h->rowptr.as<int>(), h->col.as<int>(), h->cap, h->H, h->clk.as<Clock>(),
                 h->batch_stride};
     const double hc = h->cutoff * 1.001;
-    k_broadphase<R><<<1, 1024, 0, h->stream>>>(make_dev<R>(h, h->slabs[0]), b, ss, h->origin[0],
-                                               h->origin[1], h->origin[2], (R)hc,
-                                               (R)(h->cutoff * h->cutoff));
+    {   // cooperative: all CTAs resident (grid-wide barriers between the phases)
+      Dev<R> d0 = make_dev<R>(h, h->slabs[0]);
+      double ox = h->origin[0], oy = h->origin[1], oz = h->origin[2];
+      R hr = (R)hc, c2 = (R)(h->cutoff * h->cutoff);
+      const R4* ssc = ss;
+      void* args[] = {&d0, &b, &ssc, &ox, &oy, &oz, &hr, &c2};
+      VX_CUDA(cudaLaunchCooperativeKernel((const void*)k_broadphase<R>, dim3(h->bp_grid), dim3(1024), args,
+                                          0, h->stream));
+    }
     for (size_t q = 0; q < h->slabs.size(); ++q) {
       const int s0 = h->slab_seg(q, 0), s1 = h->slab_seg(q, 1);
       if (s1 > s0)

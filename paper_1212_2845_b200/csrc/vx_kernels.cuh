@@ -12,9 +12,11 @@
 #pragma once
 #include "vx_common.cuh"
 
+#include <cooperative_groups.h>
 #include <type_traits>
 
 namespace vx {
+namespace cg = cooperative_groups;
 
 // Device-resident per-lattice scalars (one allocation).
 struct Clock {
@@ -67,8 +69,7 @@ struct ClockArgs {
   int collide, precision;
 };
 
-__global__ void k_clock(ClockArgs a) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ __forceinline__ void clock_tick(const ClockArgs& a) {
   Clock* c = a.clk;
   const long long n = c->next;
   const double t = (double)n * a.dt;
@@ -93,6 +94,10 @@ __global__ void k_clock(ClockArgs a) {
     }
     c->budget = b;
   }
+}
+__global__ void k_clock(ClockArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  clock_tick(a);
 }
 
 // ------------------------------------------------------------------ K2 dt
@@ -1174,15 +1179,63 @@ __device__ __forceinline__ void box_ijk(const Dev<R>& d, unsigned g, int& i, int
   k = (int)(r - (unsigned)j * d.nz);
 }
 
-template <class R>
-__global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, const typename VT<R>::R4* ss,
-                                                     double ox, double oy, double oz, R h, R cutoff2) {
+// Partners of surface voxel s (global surface indices u != s in the 27 cells
+// around it with |D_s - D_u| < cutoff and lattice Manhattan distance > 3):
+// counted (FILL = false) or written to col[base..) and sorted ascending.
+template <bool FILL, class R>
+__device__ __forceinline__ int bp_row(const Dev<R>& d, const BroadArgs& b,
+                                      const typename VT<R>::R4* ss, int s, R cutoff2, int base) {
   using R4 = typename VT<R>::R4;
-  if (!d.clk->rebuild) return;
-  const int T = blockDim.x, t = threadIdx.x;
-  for (int x = t; x < b.H; x += T) b.bcount[x] = 0;
-  __syncthreads();
-  for (int s = t; s < b.S; s += T) {
+  const int4 cs = b.cellh[s];
+  int ia, ja, ka;
+  box_ijk(d, b.gbox[s], ia, ja, ka);
+  const R4 pa = ss[2 * s];
+  int cnt = 0;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int cx = cs.x + dx, cy = cs.y + dy, cz = cs.z + dz;
+        const int hh = cell_hash(cx, cy, cz, b.H);
+        for (int q = b.bstart[hh]; q < b.bstart[hh + 1]; ++q) {
+          const int u = b.bitems[q];
+          const int4 cu = b.cellh[u];
+          if (u == s || cu.x != cx || cu.y != cy || cu.z != cz) continue;
+          int ib, jb, kb;
+          box_ijk(d, b.gbox[u], ib, jb, kb);
+          if (abs(ia - ib) + abs(ja - jb) + abs(ka - kb) <= 3) continue;
+          if (b.batch_stride && ia / b.batch_stride != ib / b.batch_stride) continue;
+          const R4 pb = ss[2 * u];
+          const R rx = d.l * (R)(ia - ib) + (pa.x - pb.x);
+          const R ry = d.l * (R)(ja - jb) + (pa.y - pb.y);
+          const R rz = d.l * (R)(ka - kb) + (pa.z - pb.z);
+          if (rx * rx + ry * ry + rz * rz >= cutoff2) continue;
+          if (FILL && base + cnt < b.cap) b.col[base + cnt] = u;
+          ++cnt;
+        }
+      }
+  if (FILL && base + cnt <= b.cap) {   // sort the row by partner index (deterministic)
+    for (int x = base + 1; x < base + cnt; ++x) {
+      const int v = b.col[x];
+      int y = x - 1;
+      while (y >= base && b.col[y] > v) { b.col[y + 1] = b.col[y]; --y; }
+      b.col[y + 1] = v;
+    }
+  }
+  return cnt;
+}
+
+// Cooperative launch over the whole GPU (grid-wide barriers between phases),
+// 1024 threads per CTA; every CTA returns at once unless this step rebuilds.
+// The two scans (bucket starts, row pointers) run in CTA 0.
+template <class R>
+__device__ __forceinline__ void broadphase_phases(const Dev<R>& d, const BroadArgs& b,
+                                                  const typename VT<R>::R4* ss, double ox, double oy,
+                                                  double oz, R h, R cutoff2, cg::grid_group& g) {
+  using R4 = typename VT<R>::R4;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  for (int x = tid; x < b.H; x += nth) b.bcount[x] = 0;
+  g.sync();
+  for (int s = tid; s < b.S; s += nth) {
     int i, j, k;
     box_ijk(d, b.gbox[s], i, j, k);
     const R4 p = ss[2 * s];
@@ -1194,77 +1247,41 @@ __global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, cons
     b.cellh[s] = make_int4(cx, cy, cz, hh);
     atomicAdd(&b.bcount[hh], 1);
   }
-  __syncthreads();
-  for (int x = t; x < b.H; x += T) b.bstart[x] = b.bcount[x];
-  __syncthreads();
-  cta_exscan(b.bstart, b.H);
-  for (int x = t; x < b.H; x += T) b.bcount[x] = 0;
-  __syncthreads();
-  for (int s = t; s < b.S; s += T) {
+  g.sync();
+  if (blockIdx.x == 0) {
+    for (int x = threadIdx.x; x < b.H; x += blockDim.x) b.bstart[x] = b.bcount[x];
+    __syncthreads();
+    cta_exscan(b.bstart, b.H);
+    for (int x = threadIdx.x; x < b.H; x += blockDim.x) b.bcount[x] = 0;
+  }
+  g.sync();
+  for (int s = tid; s < b.S; s += nth) {
     const int hh = b.cellh[s].w;
     b.bitems[b.bstart[hh] + atomicAdd(&b.bcount[hh], 1)] = s;
   }
-  __syncthreads();
-  // two passes: count, then fill (pass 1 writes rowptr, pass 2 col)
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int s = t; s < b.S; s += T) {
-      if (s < b.r0 || s >= b.r1) {
-        if (!pass) b.rowptr[s] = 0;
-        continue;
-      }
-      const int4 cs = b.cellh[s];
-      int ia, ja, ka;
-      box_ijk(d, b.gbox[s], ia, ja, ka);
-      const R4 pa = ss[2 * s];
-      int cnt = 0;
-      const int base = pass ? b.rowptr[s] : 0;
-      for (int dz = -1; dz <= 1; ++dz)
-        for (int dy = -1; dy <= 1; ++dy)
-          for (int dx = -1; dx <= 1; ++dx) {
-            const int cx = cs.x + dx, cy = cs.y + dy, cz = cs.z + dz;
-            const int hh = cell_hash(cx, cy, cz, b.H);
-            for (int q = b.bstart[hh]; q < b.bstart[hh + 1]; ++q) {
-              const int u = b.bitems[q];
-              const int4 cu = b.cellh[u];
-              if (u == s || cu.x != cx || cu.y != cy || cu.z != cz) continue;
-              int ib, jb, kb;
-              box_ijk(d, b.gbox[u], ib, jb, kb);
-              if (abs(ia - ib) + abs(ja - jb) + abs(ka - kb) <= 3) continue;
-              if (b.batch_stride && ia / b.batch_stride != ib / b.batch_stride) continue;
-              const R4 pb = ss[2 * u];
-              const R rx = d.l * (R)(ia - ib) + (pa.x - pb.x);
-              const R ry = d.l * (R)(ja - jb) + (pa.y - pb.y);
-              const R rz = d.l * (R)(ka - kb) + (pa.z - pb.z);
-              if (rx * rx + ry * ry + rz * rz >= cutoff2) continue;
-              if (pass) {
-                if (base + cnt < b.cap) b.col[base + cnt] = u;
-              }
-              ++cnt;
-            }
-          }
-      if (!pass) {
-        b.rowptr[s] = cnt;
-      } else if (base + cnt <= b.cap) {   // sort the row by partner index
-        for (int x = base + 1; x < base + cnt; ++x) {
-          const int v = b.col[x];
-          int y = x - 1;
-          while (y >= base && b.col[y] > v) { b.col[y + 1] = b.col[y]; --y; }
-          b.col[y + 1] = v;
-        }
-      }
-    }
-    __syncthreads();
-    if (!pass) {
-      cta_exscan(b.rowptr, b.S);
-      if (t == 0) {
-        const long long tot = b.rowptr[b.S];
-        if (tot > b.cap) d.clk->overflow = 1;
-        d.clk->npairs = tot;          // half-edges of the rows built here
-        d.clk->rebuilds += 1;
-      }
-      __syncthreads();
+  g.sync();
+  for (int s = tid; s < b.S; s += nth)
+    b.rowptr[s] = (s >= b.r0 && s < b.r1) ? bp_row<false>(d, b, ss, s, cutoff2, 0) : 0;
+  g.sync();
+  if (blockIdx.x == 0) {
+    cta_exscan(b.rowptr, b.S);
+    if (threadIdx.x == 0) {
+      const long long tot = b.rowptr[b.S];
+      if (tot > b.cap) d.clk->overflow = 1;
+      d.clk->npairs = tot;          // half-edges of the rows built here
+      d.clk->rebuilds += 1;
     }
   }
+  g.sync();
+  for (int s = tid; s < b.S; s += nth)
+    if (s >= b.r0 && s < b.r1) bp_row<true>(d, b, ss, s, cutoff2, b.rowptr[s]);
+}
+template <class R>
+__global__ void __launch_bounds__(1024, 1) k_broadphase(Dev<R> d, BroadArgs b, const typename VT<R>::R4* ss,
+                                                     double ox, double oy, double oz, R h, R cutoff2) {
+  if (!d.clk->rebuild) return;
+  cg::grid_group g = cg::this_grid();
+  broadphase_phases(d, b, ss, ox, oy, oz, h, cutoff2, g);
 }
 
 // ------------------------------------------------------------------ contact
@@ -1273,12 +1290,10 @@ __global__ void __launch_bounds__(1024) k_broadphase(Dev<R> d, BroadArgs b, cons
 // (= ascending box id).  Rows [r0, r1) are one slab's segment; the load goes
 // to that slab's cf at the voxel's local id.
 template <class R>
-__global__ void __launch_bounds__(256) k_contact(Dev<R> d, const unsigned* gbox,
-                                                 const typename VT<R>::R4* ss, int r0, int r1,
-                                                 const int* rowptr, const int* col, R zeta_col) {
+__device__ __forceinline__ void contact_row(const Dev<R>& d, const unsigned* gbox,
+                                            const typename VT<R>::R4* ss, int s, const int* rowptr,
+                                            const int* col, R zeta_col) {
   using R4 = typename VT<R>::R4;
-  const int s = r0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= r1) return;
   int ia, ja, ka;
   box_ijk(d, gbox[s], ia, ja, ka);
   const R4 pa = ss[2 * s];
@@ -1315,6 +1330,13 @@ __global__ void __launch_bounds__(256) k_contact(Dev<R> d, const unsigned* gbox,
     F = F + f * n;
   }
   d.cf[gbox[s] - (unsigned)d.xl0 * d.sx] = R4{F.x, F.y, F.z, R(0)};
+}
+template <class R>
+__global__ void __launch_bounds__(256) k_contact(Dev<R> d, const unsigned* gbox,
+                                                 const typename VT<R>::R4* ss, int r0, int r1,
+                                                 const int* rowptr, const int* col, R zeta_col) {
+  const int s = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < r1) contact_row(d, gbox, ss, s, rowptr, col, zeta_col);
 }
 
 // ------------------------------------------------------------------ state I/O
