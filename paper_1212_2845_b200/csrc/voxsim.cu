@@ -164,6 +164,7 @@ struct vx_lattice {
   int fused_ty = 8;                       // rows per fused block (VX_FUSED_TY overrides)
   int fused_waves = 4;                    // block waves per fused launch (VX_FUSED_WAVES)
   int fused_tune = 1;                     // time candidate segment lengths once (VX_FUSED_TUNE)
+  int fused_sx = 0;                       // fixed planes per segment (VX_FUSED_SX), 0: derived
   std::map<long long, std::pair<int, int>> geo_tuned;   // (TY, SX) chosen per launch range
   int batch_stride = 0;                   // planes per batched scene (vx_set_batch)
 
@@ -579,16 +580,15 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
     const int planes = e - b;
     if (planes < 1) continue;
     const bool big = (long long)planes * h->plane >= (1LL << 22);
-    static const int ty_big[] = {6, 8}, ty_small[] = {1, 2, 4, 8};
+    static const int ty_big[] = {4, 5, 6, 7, 8}, ty_small[] = {1, 2, 4, 8};
     static const int sx_big[] = {3, 4, 5, 6, 7, 8, 10, 12, 14, 16, 20, 24, 32};
     static const int sx_small[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
     const int* tys = big ? ty_big : ty_small;
-    const int nty = big ? 2 : 4;
+    const int nty = big ? 5 : 4;
     const int* sxs = big ? sx_big : sx_small;
     const int nsx = big ? 13 : 10;
     const int reps = big ? 3 : 8;
-    float best = 1e30f;
-    std::pair<int, int> best_g{0, 0};
+    std::vector<std::pair<float, std::pair<int, int>>> times;
     for (int a = 0; a < nty; ++a) {
       const int ty = tys[a];
       if (ty > h->ny && ty != tys[0]) break;
@@ -602,10 +602,28 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
         VX_CUDA(cudaEventSynchronize(e1));
         float ms = 0;
         VX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        if (ms < best) { best = ms; best_g = {ty, sx}; }
+        times.push_back({ms, {ty, sx}});
       }
     }
-    if (best_g.first) h->geo_tuned[fused_key(s, b, e)] = best_g;
+    if (times.empty()) continue;
+    // fastest, except that a smaller TY within 1.5 % of it wins: shorter row
+    // tiles re-read fewer neighbour rows from DRAM (profiles/r09_geometry.md)
+    float best = 1e30f;
+    for (auto& c : times) best = std::min(best, c.first);
+    std::pair<int, int> best_g{0, 0};
+    float best_t = 1e30f;
+    for (auto& c : times) {
+      if (c.first > 1.015f * best) continue;
+      if (!best_g.first || c.second.first < best_g.first ||
+          (c.second.first == best_g.first && c.first < best_t)) {
+        best_g = c.second;
+        best_t = c.first;
+      }
+    }
+    h->geo_tuned[fused_key(s, b, e)] = best_g;
+    if (std::getenv("VX_FUSED_TUNE_LOG"))
+      std::fprintf(stderr, "voxsim: fused geometry for planes [%d, %d): TY=%d SX=%d (%.3f ms / launch)\n", b, e,
+                   best_g.first, best_g.second, best_t / reps);
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -651,6 +669,7 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
   a.sx = (planes + nseg - 1) / nseg;
   if (sx_force > 0) a.sx = std::min(sx_force, planes);
   else if (have) a.sx = std::min(tuned->second.second, planes);
+  else if (h->fused_sx > 0) a.sx = std::min(h->fused_sx, planes);
   const int segs = (planes + a.sx - 1) / a.sx;
   const int pi = sizeof(R) == 4 ? 0 : 1;
   if (!h->fused_smem_set[pi]) {
@@ -1042,6 +1061,10 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   }
   if (const char* e = std::getenv("VX_FUSED_WAVES")) {
     h->fused_waves = std::max(1, std::min(64, std::atoi(e)));
+    h->fused_tune = 0;
+  }
+  if (const char* e = std::getenv("VX_FUSED_SX")) {   // planes per segment (experiments)
+    h->fused_sx = std::max(1, std::min(512, std::atoi(e)));
     h->fused_tune = 0;
   }
   if (const char* e = std::getenv("VX_FUSED_TUNE")) h->fused_tune = std::atoi(e);
