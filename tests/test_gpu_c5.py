@@ -99,3 +99,14 @@ def test_c5_full_size_sampled_one_step(engine):
     assert latch_ok == len(pts)
     assert eP <= 1e-4 and eD <= 1e-4, (eP, eD)
     assert ephi <= 1e-3, ephi
+
+
+def test_c5_runs_its_1000_steps():
+    """C5 as specified (1k steps, BASELINE.json configs[4]) completes without a
+    divergence at zeta_b = 0.9 (R20: zeta_b = 1 is marginally unstable
+    for this recipe in the fp64 oracle as well)."""
+    sc = W.block(precision=32)
+    lat = from_scene(sc, precision=32, init_state=False, engine="fused")
+    lat.step(sc.steps)
+    st = lat.read_voxels(np.arange(0, NX * NY * NZ, 4099))
+    assert np.all(np.isfinite(st.pos)) and np.abs(st.linmom).max() < 1e-6
