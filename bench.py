@@ -262,9 +262,11 @@ def run_ours(args):
     barrier()
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
+    n_instr = args.steps
     if not live:
+        n_instr = min(args.steps, 50)
         lat.set_instrumentation(True)
-        lat.step(min(args.steps, 50))
+        lat.step(n_instr)
     kt = lat.kernel_times()
     lat.set_instrumentation(False)
     ms_max = vd.max_over_ranks([ms], dist if world > 1 else None, "cuda")[0]
@@ -278,7 +280,7 @@ def run_ours(args):
     kinds = ("fused",) if fused else ("bonds", "integrate")
     slot = {"fused": "integrate", "bonds": "bonds", "integrate": "integrate"}
     avg = {k: kt[slot[k]][0] / max(kt[slot[k]][1], 1) for k in kinds}
-    per_step_ms = {k: kt[slot[k]][0] / args.steps for k in kinds}
+    per_step_ms = {k: kt[slot[k]][0] / n_instr for k in kinds}
     dom = max(per_step_ms, key=per_step_ms.get)
     peak, peak_src = _peaks()
     gbps = {k: alg[k] * vox_rank / (per_step_ms[k] / 1e3) / 1e9 for k in kinds}

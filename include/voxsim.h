@@ -201,13 +201,13 @@ int64_t vx_contact_pairs(vx_lattice* h, int64_t* pairs, int64_t cap);
  * Owned by the library; valid until vx_destroy. */
 void* vx_stream(const vx_lattice* h);
 
-/* Kernel-level instrumentation.  When on, vx_step launches without CUDA
- * graphs and brackets every launch of the bond kernel (K3) and the
- * gather-integrate kernel (K4) with CUDA events on vx_stream();
- * vx_kernel_times returns, since the last reset, the summed device time in ms
- * and the launch count of each kernel class:
- * out_ms[0]/counts[0] = K3 bonds, [1] = K4 gather-integrate, [2] = other
- * (clock, broadphase, contact), [3] = all kernels. */
+/* Kernel-level instrumentation.  When on, the CUDA graphs vx_step replays
+ * carry CUDA event-record nodes around every launch class of every step (on
+ * vx_stream()), read back after each graph replay; vx_kernel_times returns,
+ * since the last reset, the summed device time in ms and the launch count of
+ * each kernel class: out_ms[0]/counts[0] = K3 bonds, [1] = K4
+ * gather-integrate or the fused pass, [2] = other (clock, surface table,
+ * broadphase, contact, ghost-plane copies), [3] = the whole step. */
 vx_status vx_set_instrumentation(vx_lattice* h, int32_t on);
 vx_status vx_kernel_times(vx_lattice* h, double out_ms[4], int64_t counts[4]);
 /* Number of kernels vx_step launches per step with the current settings. */

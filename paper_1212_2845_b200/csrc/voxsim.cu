@@ -588,6 +588,16 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
     const int* sxs = big ? sx_big : sx_small;
     const int nsx = big ? 13 : 10;
     const int reps = big ? 3 : 8;
+    auto time_geo = [&](int ty, int sx, int nrep, float* ms) -> vx_status {
+      VX_TRY(launch_fused<R>(h, s, col, b, e, sx, nullptr, 0, 0, ty));   // warm
+      VX_CUDA(cudaEventRecord(e0, h->stream));
+      for (int r = 0; r < nrep; ++r) VX_TRY(launch_fused<R>(h, s, col, b, e, sx, nullptr, 0, 0, ty));
+      VX_CUDA(cudaEventRecord(e1, h->stream));
+      VX_CUDA(cudaEventSynchronize(e1));
+      VX_CUDA(cudaEventElapsedTime(ms, e0, e1));
+      *ms /= (float)nrep;
+      return VX_OK;
+    };
     std::vector<std::pair<float, std::pair<int, int>>> times;
     for (int a = 0; a < nty; ++a) {
       const int ty = tys[a];
@@ -595,25 +605,24 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
       for (int c = 0; c < nsx; ++c) {
         const int sx = sxs[c];
         if (sx > planes && c > 0) break;
-        VX_TRY(launch_fused<R>(h, s, col, b, e, sx, nullptr, 0, 0, ty));   // warm
-        VX_CUDA(cudaEventRecord(e0, h->stream));
-        for (int r = 0; r < reps; ++r) VX_TRY(launch_fused<R>(h, s, col, b, e, sx, nullptr, 0, 0, ty));
-        VX_CUDA(cudaEventRecord(e1, h->stream));
-        VX_CUDA(cudaEventSynchronize(e1));
         float ms = 0;
-        VX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        VX_TRY(time_geo(ty, sx, reps, &ms));
         times.push_back({ms, {ty, sx}});
       }
     }
     if (times.empty()) continue;
-    // fastest, except that a smaller TY within 1.5 % of it wins: shorter row
-    // tiles re-read fewer neighbour rows from DRAM (profiles/r09_geometry.md)
+    // second round: the six fastest re-timed with three times the repetitions
+    std::sort(times.begin(), times.end());
+    if (times.size() > 6) times.resize(6);
+    for (auto& c : times) VX_TRY(time_geo(c.second.first, c.second.second, 3 * reps, &c.first));
+    // fastest; a smaller TY within 0.3 % (a tie) wins: shorter row tiles re-read
+    // fewer neighbour rows from DRAM (profiles/r09_geometry.md)
     float best = 1e30f;
     for (auto& c : times) best = std::min(best, c.first);
     std::pair<int, int> best_g{0, 0};
     float best_t = 1e30f;
     for (auto& c : times) {
-      if (c.first > 1.015f * best) continue;
+      if (c.first > 1.003f * best) continue;
       if (!best_g.first || c.second.first < best_g.first ||
           (c.second.first == best_g.first && c.first < best_t)) {
         best_g = c.second;
@@ -623,7 +632,7 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
     h->geo_tuned[fused_key(s, b, e)] = best_g;
     if (std::getenv("VX_FUSED_TUNE_LOG"))
       std::fprintf(stderr, "voxsim: fused geometry for planes [%d, %d): TY=%d SX=%d (%.3f ms / launch)\n", b, e,
-                   best_g.first, best_g.second, best_t / reps);
+                   best_g.first, best_g.second, best_t);
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -775,7 +784,7 @@ vx_status halo_local(vx_lattice* h) {
 
 template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
   const bool col = h->collide();
-  if (ev) VX_CUDA(cudaEventRecord(ev[0], h->stream));
+  if (ev) VX_CUDA(cudaEventRecordWithFlags(ev[0], h->stream, cudaEventRecordExternal));
   ClockArgs ca{h->clk.as<Clock>(), h->dt, h->env.T_amp, h->env.T_freq, h->env.T_phase,
                0.5 * h->env.horizon_voxels * h->l, h->alpha_lo, h->alpha_hi, col ? 1 : 0,
                h->prec};
@@ -828,7 +837,8 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
     }
   }
   if (h->emulated) VX_TRY(halo_local(h));
-  if (ev) VX_CUDA(cudaEventRecord(ev[1], h->stream));
+  // (the fused engine has no bond-kernel interval: ev[1] would sit next to ev[2])
+  if (ev && !h->fused()) VX_CUDA(cudaEventRecordWithFlags(ev[1], h->stream, cudaEventRecordExternal));
   if (h->fused()) {
     if (h->nccl()) {
       // ghost planes of S_n on the comm stream, overlapped with the interior
@@ -839,13 +849,13 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
       VX_CUDA(cudaEventRecord(h->ev_k4, h->stream));
       VX_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_k4, 0));
       VX_TRY(halo_nccl(h));
-      if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
+      if (ev) VX_CUDA(cudaEventRecordWithFlags(ev[2], h->stream, cudaEventRecordExternal));
       VX_TRY(launch_fused<R>(h, s, col, s.x0 + 1, s.x1 - 1));
       VX_TRY(launch_boundary<R>(h, s, col, h->comm_stream));
       VX_CUDA(cudaEventRecord(h->ev_halo, h->comm_stream));
       VX_CUDA(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
     } else {
-      if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
+      if (ev) VX_CUDA(cudaEventRecordWithFlags(ev[2], h->stream, cudaEventRecordExternal));
       for (const Slab& s : h->slabs) {
         if (h->emulated) {   // the launch split of the NCCL ranks (ghosts already copied)
           VX_TRY(launch_fused<R>(h, s, col, s.x0 + 1, s.x1 - 1));
@@ -855,7 +865,7 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
         }
       }
     }
-    if (ev) VX_CUDA(cudaEventRecord(ev[3], h->stream));
+    if (ev) VX_CUDA(cudaEventRecordWithFlags(ev[3], h->stream, cudaEventRecordExternal));
     VX_CUDA(cudaGetLastError());
     h->flip();
     return VX_OK;
@@ -875,54 +885,40 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
   } else {
     for (const Slab& s : h->slabs) launch_bonds<R>(h, s, make_dev<R>(h, s), s.xl0, s.x1);
   }
-  if (ev) VX_CUDA(cudaEventRecord(ev[2], h->stream));
+  if (ev) VX_CUDA(cudaEventRecordWithFlags(ev[2], h->stream, cudaEventRecordExternal));
   for (const Slab& s : h->slabs) launch_integrate<R>(h, s, make_dev<R>(h, s), col);
-  if (ev) VX_CUDA(cudaEventRecord(ev[3], h->stream));
+  if (ev) VX_CUDA(cudaEventRecordWithFlags(ev[3], h->stream, cudaEventRecordExternal));
   VX_CUDA(cudaGetLastError());
   return VX_OK;
 }
 
 template <class R> vx_status run_steps(vx_lattice* h, long long n) {
   VX_TRY(tune_fused<R>(h));
+  // CUDA graphs of G steps; the remainder is captured as its own graph.  The
+  // fused engine ping-pongs two state copies, so a graph also depends on which
+  // copy is current when it starts (key = 2 g + parity).  With instrumentation
+  // on, the graphs carry event-record nodes around every launch class of every
+  // step (their own cache); the times are read after each graph replay.
+  const long long G = 32;
   if (h->instr) {
-    const size_t need = (size_t)n * 4;
-    while (h->events.size() < need) {
+    while (h->events.size() < (size_t)G * 4) {
       cudaEvent_t e;
       VX_CUDA(cudaEventCreate(&e));
       h->events.push_back(e);
     }
-    for (long long s = 0; s < n; ++s) VX_TRY(enqueue_step<R>(h, &h->events[(size_t)s * 4]));
-    VX_CUDA(cudaStreamSynchronize(h->stream));
-    for (long long s = 0; s < n; ++s) {
-      cudaEvent_t* e = &h->events[(size_t)s * 4];
-      float a, b, c, t;
-      VX_CUDA(cudaEventElapsedTime(&a, e[1], e[2]));
-      VX_CUDA(cudaEventElapsedTime(&b, e[2], e[3]));
-      VX_CUDA(cudaEventElapsedTime(&c, e[0], e[1]));
-      VX_CUDA(cudaEventElapsedTime(&t, e[0], e[3]));
-      h->t_ms[0] += a; h->t_ms[1] += b; h->t_ms[2] += c; h->t_ms[3] += t;
-      h->t_cnt[0] += h->fused() ? 0 : h->bond_launches();
-      h->t_cnt[1] += h->fused() ? h->fused_launches() : (long long)h->slabs.size();
-      h->t_cnt[2] += h->other_launches();
-      h->t_cnt[3] += h->launches_per_step();
-    }
-    return VX_OK;
   }
-  // CUDA graphs of G steps; the remainder is captured as its own graph.  The
-  // fused engine ping-pongs two state copies, so a graph also depends on which
-  // copy is current when it starts (key = 2 g + parity).
-  const long long G = 32;
   long long left = n;
   while (left > 0) {
     const long long g = left >= G ? G : left;
     const int par = h->slabs[0].par;
-    const long long key = 2 * g + (h->fused() ? par : 0);
+    const long long key = 2 * g + (h->fused() ? par : 0) + (h->instr ? (1LL << 40) : 0);
     auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {
       cudaGraph_t graph;
       VX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
       vx_status st = VX_OK;
-      for (long long s = 0; s < g && st == VX_OK; ++s) st = enqueue_step<R>(h, nullptr);
+      for (long long s = 0; s < g && st == VX_OK; ++s)
+        st = enqueue_step<R>(h, h->instr ? &h->events[(size_t)s * 4] : nullptr);
       cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
       for (auto& s : h->slabs) s.par = par;   // capture only recorded the flips
       if (st != VX_OK) return st;
@@ -935,6 +931,26 @@ template <class R> vx_status run_steps(vx_lattice* h, long long n) {
     VX_CUDA(cudaGraphLaunch(it->second, h->stream));
     if (h->fused() && (g & 1)) h->flip();
     left -= g;
+    if (h->instr) {
+      VX_CUDA(cudaStreamSynchronize(h->stream));
+      for (long long s = 0; s < g; ++s) {
+        cudaEvent_t* e = &h->events[(size_t)s * 4];
+        float a = 0, b, c, t;
+        if (h->fused()) {
+          VX_CUDA(cudaEventElapsedTime(&c, e[0], e[2]));
+        } else {
+          VX_CUDA(cudaEventElapsedTime(&a, e[1], e[2]));
+          VX_CUDA(cudaEventElapsedTime(&c, e[0], e[1]));
+        }
+        VX_CUDA(cudaEventElapsedTime(&b, e[2], e[3]));
+        VX_CUDA(cudaEventElapsedTime(&t, e[0], e[3]));
+        h->t_ms[0] += a; h->t_ms[1] += b; h->t_ms[2] += c; h->t_ms[3] += t;
+        h->t_cnt[0] += h->fused() ? 0 : h->bond_launches();
+        h->t_cnt[1] += h->fused() ? h->fused_launches() : (long long)h->slabs.size();
+        h->t_cnt[2] += h->other_launches();
+        h->t_cnt[3] += h->launches_per_step();
+      }
+    }
   }
   VX_CUDA(cudaStreamSynchronize(h->stream));
   return VX_OK;
