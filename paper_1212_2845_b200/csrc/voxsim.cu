@@ -580,11 +580,11 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
     const int planes = e - b;
     if (planes < 1) continue;
     const bool big = (long long)planes * h->plane >= (1LL << 22);
-    static const int ty_big[] = {4, 5, 6, 7, 8}, ty_small[] = {1, 2, 4, 8};
+    static const int ty_big[] = {4, 5, 6, 7, 8}, ty_small[] = {1, 2, 4, 5, 6, 7, 8};
     static const int sx_big[] = {3, 4, 5, 6, 7, 8, 10, 12, 14, 16, 20, 24, 32};
     static const int sx_small[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
     const int* tys = big ? ty_big : ty_small;
-    const int nty = big ? 5 : 4;
+    const int nty = big ? 5 : 7;
     const int* sxs = big ? sx_big : sx_small;
     const int nsx = big ? 13 : 10;
     const int reps = big ? 3 : 8;
