@@ -519,6 +519,20 @@ vx_status setup_collision(vx_lattice* h) {
 }
 
 vx_status prepare(vx_lattice* h) {
+  if (!h->fused()) {   // bond records (K3 -> K4), allocated on the first two-pass step
+    const size_t r = rsize(h->prec);
+    for (Slab& sl : h->slabs) {
+      if (sl.recA.p) continue;
+      const size_t n = sl.nloc;
+      VX_TRY(sl.recA.alloc(3 * n * 4 * r));
+      VX_TRY(sl.recB.alloc(3 * n * 4 * r));
+      VX_TRY(sl.recC.alloc(3 * n * r));
+      VX_CUDA(cudaMemset(sl.recA.p, 0, sl.recA.bytes));
+      VX_CUDA(cudaMemset(sl.recB.p, 0, sl.recB.bytes));
+      VX_CUDA(cudaMemset(sl.recC.p, 0, sl.recC.bytes));
+      h->clear_graphs();
+    }
+  }
   if (!h->mats_set) return fail(VX_ERR_STATE, "vx_set_materials has not been called");
   if (!h->env_set) return fail(VX_ERR_STATE, "vx_set_environment has not been called");
   if (h->tables_dirty) {
@@ -1115,14 +1129,12 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   for (Slab& sl : h->slabs) {
     const size_t n = sl.nloc;
     if ((s = sl.pos().alloc(n * 4 * r)) || (s = sl.quat().alloc(n * 4 * r)) || (s = sl.mom().alloc(n * 4 * r)) ||
-        (s = sl.ang().alloc(n * 2 * r)) || (s = sl.recA.alloc(3 * n * 4 * r)) ||
-        (s = sl.recB.alloc(3 * n * 4 * r)) || (s = sl.recC.alloc(3 * n * r)) ||
+        (s = sl.ang().alloc(n * 2 * r)) ||
         (s = sl.meta_d.alloc(n * 4)) || (s = sl.ext_of_local.alloc(n * 4)))
       return bail(s);
     // initial state: at rest on the lattice sites, identity orientation (.w = 1)
     if (cudaMemset(sl.pos().p, 0, sl.pos().bytes) != cudaSuccess || cudaMemset(sl.mom().p, 0, sl.mom().bytes) != cudaSuccess ||
-        cudaMemset(sl.ang().p, 0, sl.ang().bytes) != cudaSuccess || cudaMemset(sl.recA.p, 0, sl.recA.bytes) != cudaSuccess ||
-        cudaMemset(sl.recB.p, 0, sl.recB.bytes) != cudaSuccess || cudaMemset(sl.recC.p, 0, sl.recC.bytes) != cudaSuccess)
+        cudaMemset(sl.ang().p, 0, sl.ang().bytes) != cudaSuccess)
       return bail(fail(VX_ERR_CUDA, "memset failed"));
     std::vector<char> q(sl.quat().bytes, 0);
     for (size_t i = 0; i < n; ++i) {
