@@ -89,3 +89,26 @@ def test_bond_damping_noise_floor_fp32():
         jitter[zb] = np.max(np.abs(np.array(z) - z[-1]))
     assert jitter[0.0] > 0
     assert jitter[1.0] <= 1e-4 * jitter[0.0], jitter      # SPEC AC4 (paper: ~1e-7)
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_clapper_scheme_equivalence(prec):
+    """a clapper-like +-CTE scene whose two arms close on
+    each other.  The GPU runs the horizon scheme (surface voxels, hashed grid,
+    rebuild on the motion budget); the oracle runs all pairs every
+    step (A22).  Same contacts, same state."""
+    from parity import errors, run_pair
+    sc = W.clapper()
+    g, o, p0, lat, orc = run_pair(sc, sc.steps, prec, chunks=6)
+    e = errors(g, o, p0, sc.lattice_dim)
+    assert e["eD"] <= {64: 1e-9, 32: 1e-4}[prec], e
+    ijk = sc.voxel_coords()
+    tip_a = (ijk[:, 0] == 13) & (ijk[:, 2] == 1)
+    tip_b = (ijk[:, 0] == 13) & (ijk[:, 2] == 5)
+    gap = g.pos[tip_b, 2].min() - g.pos[tip_a, 2].max()
+    assert gap < sc.lattice_dim                        # the arms touch ...
+    assert gap > 0.9 * sc.lattice_dim                  # ... without passing through
+    assert lat.num_rebuilds >= 2
+    ov = {tuple(p) for p in orc.contact_pairs()}       # overlapping pairs (oracle)
+    sl = {tuple(p) for p in lat.contact_pairs()}       # the GPU's shortlist covers them
+    assert ov and ov <= sl

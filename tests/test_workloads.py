@@ -56,3 +56,11 @@ def test_sphere_and_walker_geometry():
     assert pos[:, 2].min() - 0.5 * s.lattice_dim == pytest.approx(0.5 * s.lattice_dim)
     w = W.walker()
     assert np.all(w.cells[:4] == 1) and set(np.unique(w.cells[4:])) == {2, 3}
+
+
+def test_clapper_recipe():
+    s = W.clapper()
+    assert s.cells.shape == (7, 2, 14) and s.num_voxels == 118
+    assert int(s.fixed.sum()) == 14                     # the base column
+    ctes = sorted(m["cte"] for m in s.materials)
+    assert ctes == [-0.002, 0.0, 0.002] and s.env["self_collision"] == 1

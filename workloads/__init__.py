@@ -184,6 +184,28 @@ def two_bodies(n=3, gap=2, v=2.0, E=1e6):
     return s
 
 
+def clapper(n=13, gap=3, cte=0.002, dT=10.0):
+    """A clapper-like +-CTE scene: two bimorph strips of
+    n x 2 x 2 voxels, `gap` voxels apart in z, held by a fixed base column at
+    x = 0.  Strip A (bottom) is +CTE under -CTE and curls up, strip B (top)
+    the mirror image; a constant temperature rise dT (T = T_amp sin(pi/2))
+    closes them onto each other: surface self contact between the two arms."""
+    nz = 4 + gap
+    cells = np.zeros((nz, 2, n + 1), np.uint8)
+    cells[:, :, 0] = 1                                # base column (passive, fixed)
+    cells[0, :, 1:] = 2                               # strip A: +CTE below ...
+    cells[1, :, 1:] = 3                               # ... -CTE above -> curls toward B
+    cells[nz - 2, :, 1:] = 3                          # strip B: -CTE below ...
+    cells[nz - 1, :, 1:] = 2                          # ... +CTE above -> curls toward A
+    mats = [_mat(1e6, 1000.0), _mat(1e6, 1000.0, cte=cte), _mat(1e6, 1000.0, cte=-cte)]
+    env = _env(zeta_bond=1.0, zeta_col=0.5, self_collision=1, horizon_voxels=2.0,
+               T_amp=dT, T_freq=0.0, T_phase=float(np.pi / 2))
+    s = Scene("clapper", cells, L, mats, env, steps=3000,
+              notes="constant dT via T_phase = pi/2; base column fixed")
+    s.fixed = (s.voxel_coords()[:, 0] == 0).astype(np.uint8)
+    return s
+
+
 def app_a_beam():
     """E9: App. A listing: 5x10x5 of 10 MPa, nu 0.3, -Y plane fixed,
     1 kN spread over the +Y plane, SetSlowDampZ(0.013), 400 steps.  Regions
