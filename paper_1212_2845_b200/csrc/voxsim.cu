@@ -173,7 +173,8 @@ struct vx_lattice {
   void flip() {
     for (auto& s : slabs) s.par ^= 1;
   }
-  bool nccl() const { return nranks > 1 && !emulated; }
+  bool force_nccl = false;                // VX_FORCE_NCCL: the NCCL code path with one rank (tests)
+  bool nccl() const { return (nranks > 1 && !emulated) || force_nccl; }
   bool collide() const { return env_set && env.self_collision && nsurf > 0; }
   // surface rows this handle builds: its rank's segment over NCCL, else all
   int rows_begin() const { return nccl() ? seg[rank] : 0; }
@@ -1084,6 +1085,11 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   h->prec = desc->precision;
   h->device = desc->device; h->rank = desc->rank; h->nranks = desc->nranks;
   h->emulated = emulated;
+  // one rank with a unique id and VX_FORCE_NCCL=1: every NCCL call of the slab
+  // path runs (an empty ghost exchange, one-rank broadcasts / reductions), so a
+  // single GPU exercises the multi-rank code: communicator, comm-stream overlap,
+  // NCCL inside CUDA graphs
+  if (desc->nranks == 1 && desc->nccl_id && std::getenv("VX_FORCE_NCCL")) h->force_nccl = true;
   if (const char* e = std::getenv("VX_FUSED_TMA")) h->tma_ok = std::atoi(e) != 0;
   if (const char* e = std::getenv("VX_FUSED_TY")) {
     h->fused_ty = std::max(1, std::min(64, std::atoi(e)));
