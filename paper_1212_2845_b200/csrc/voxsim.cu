@@ -147,6 +147,8 @@ struct vx_lattice {
   int bp_grid = 1;                        // CTAs of the cooperative broadphase
   long long cap = 0;
   double cutoff = 0;
+  // staging of the external fp64 state (vx_set_state / vx_read_state), kept between calls
+  DevBuf stage_ext, stage_box;
   // graphs
   std::map<long long, cudaGraphExec_t> graphs;
   // instrumentation
@@ -1293,7 +1295,7 @@ vx_status vx_set_state(vx_lattice* h, const double* pos, const double* quat, con
   VX_TRY(set_device(h));
   const long long N = h->N;
   if (N == 0) return VX_OK;
-  DevBuf b;
+  DevBuf& b = h->stage_ext;   // kept: state I/O every episode must not pay cudaMalloc / cudaFree
   const size_t off[5] = {0, (size_t)N * 3, (size_t)N * 7, (size_t)N * 10, (size_t)N * 13};
   VX_TRY(b.alloc((size_t)N * 13 * 8 + (size_t)N));
   double* bd = b.as<double>();
@@ -1436,7 +1438,8 @@ vx_status vx_read_state(vx_lattice* h, double* pos, double* quat, double* lin, d
   VX_TRY(set_device(h));
   const long long N = h->N;
   if (N == 0) return VX_OK;
-  DevBuf box, ext;
+  DevBuf& box = h->stage_box;
+  DevBuf& ext = h->stage_ext;
   VX_TRY(box.alloc((size_t)h->nbox * 14 * 8));
   VX_TRY(ext.alloc((size_t)N * 13 * 8 + (size_t)N));
   VX_TRY(read_box(h, box.as<double>()));
