@@ -815,13 +815,18 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
         nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
       VS<R> vx;
       if (FULL || (meta & nb_bit(1))) vx = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + sx);
-      // the +x row two rows ahead (first touch: HBM) into L2
-      if ((FULL || act) && j + 2 < j1 && i + 1 < a.nplanes) {
-        const uint32_t f = id + sx + 2 * nz;
-        prefetch_l2(d.pos + f);
-        prefetch_l2(d.quat + f);
-        prefetch_l2(d.mom + f);
-        prefetch_l2(d.ang + f);
+      // the +x row two rows ahead (first touch: HBM) into L2, continuing into the
+      // next plane of the segment at the end of the tile
+      if (FULL || act) {
+        int jj = j + 2, ii = i + 1;
+        if (jj >= j1) { jj -= j1 - j0; ++ii; }
+        if (ii < a.nplanes && (ii == i + 1 || i + 1 < i1)) {
+          const uint32_t f = idx(ii, jj);
+          prefetch_l2(d.pos + f);
+          prefetch_l2(d.quat + f);
+          prefetch_l2(d.mom + f);
+          prefetch_l2(d.ang + f);
+        }
       }
       VS<R> vz = vs_shfl_down(cur);
       if (lane == 31 && (meta & nb_bit(5))) {
