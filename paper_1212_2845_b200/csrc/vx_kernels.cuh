@@ -718,6 +718,9 @@ template <class R> struct FusedArgs {
   int nplanes;      // planes in the local box
 };
 
+#ifndef VX_PF_DIST
+#define VX_PF_DIST 1
+#endif
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -815,10 +818,10 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
         nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
       VS<R> vx;
       if (FULL || (meta & nb_bit(1))) vx = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + sx);
-      // the +x row two rows ahead (first touch: HBM) into L2, continuing into the
+      // the +x row VX_PF_DIST rows ahead (first touch: HBM) into L2, continuing into the
       // next plane of the segment at the end of the tile
       if (FULL || act) {
-        int jj = j + 2, ii = i + 1;
+        int jj = j + VX_PF_DIST, ii = i + 1;
         if (jj >= j1) { jj -= j1 - j0; ++ii; }
         if (ii < a.nplanes && (ii == i + 1 || i + 1 < i1)) {
           const uint32_t f = idx(ii, jj);
