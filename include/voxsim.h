@@ -218,9 +218,10 @@ int32_t vx_launches_per_step(const vx_lattice* h);
  * … calculated separately, then … summed"; 384 B/voxel-step in fp32).
  * VX_ENGINE_FUSED: one kernel per step sweeps x-planes, keeps every bond's
  * loads on chip and writes S_{n+1} to a second state copy (112 B/voxel-step);
- * same arithmetic per bond and per voxel, same summation order.  Needs
- * nz <= 256 (INVALID_ARG otherwise).  In kernel timing (vx_kernel_times) the
- * fused kernel is reported in slot [1]. */
+ * same arithmetic per bond and per voxel, same summation order.  Any nz
+ * (taller than 256: z chunks of 256 voxels, each recomputing the -z bond of
+ * its lowest layer).  In kernel timing (vx_kernel_times) the fused kernel is
+ * reported in slot [1]. */
 typedef enum { VX_ENGINE_TWO_PASS = 0, VX_ENGINE_FUSED = 1 } vx_engine;
 
 /* Batched independent scenes (the design-automation use of

@@ -171,7 +171,7 @@ struct vx_lattice {
   int batch_stride = 0;                   // planes per batched scene (vx_set_batch)
 
   bool fused() const { return engine == VX_ENGINE_FUSED; }
-  bool fused_supported() const { return nz <= 256; }
+  bool fused_supported() const { return true; }   // any nz (z chunks of 256)
   void flip() {
     for (auto& s : slabs) s.par ^= 1;
   }
@@ -660,7 +660,7 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
 }
 
 // Fused single pass over a slab's owned planes: S_n (current copy) -> S_{n+1}
-// (other copy).  Block = one thread per z (nz <= 256) x TY rows x SX planes.
+// (other copy).  Block = one thread per z (a chunk of <= 256) x TY rows x SX planes.
 template <class R>
 vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int x_end, int sx_force,
                        cudaStream_t st, int x_begin2, int x_end2, int ty_force) {
@@ -676,10 +676,13 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
   a.p0 = x_begin - s.xl0;
   a.p1 = x_end - s.xl0;
   a.nplanes = s.xl1 - s.xl0;
-  const int threads = ((h->nz + 31) / 32) * 32;
+  // one thread per z, in chunks of at most 256 (taller lattices: several z
+  // chunks, each recomputing its lowest -z bond)
+  const int threads = std::min(256, ((h->nz + 31) / 32) * 32);
+  a.zchunks = (h->nz + threads - 1) / threads;
   // TMA-staged rows need 16-byte aligned rows of every array (nz even); the
   // rows per block are the most that keep two blocks per SM in shared memory.
-  const bool tma = h->tma_ok && (h->nz % 2 == 0);
+  const bool tma = h->tma_ok && (h->nz % 2 == 0) && a.zchunks == 1;
   // rows per block and planes per segment: forced (tuning, boundary planes),
   // tuned for this range, or the defaults
   const auto tuned = h->geo_tuned.find(fused_key(s, x_begin, x_end));
@@ -699,18 +702,20 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
   const int segs = (planes + a.sx - 1) / a.sx;
   const int pi = sizeof(R) == 4 ? 0 : 1;
   if (!h->fused_smem_set[pi]) {
-    VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     VX_CUDA(cudaFuncSetAttribute(k_step_fused_tma<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     VX_CUDA(cudaFuncSetAttribute(k_step_fused_tma<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     if (const char* e = std::getenv("VX_CARVEOUT")) {   // experiment: smem carveout percent
       const int pct = std::atoi(e);
-      VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-      VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+      VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+      VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     }
     h->fused_smem_set[pi] = true;
   }
-  a.nblk0 = a.ntiles_y * segs;
+  a.nblk0 = a.ntiles_y * segs * a.zchunks;
   a.p0b = a.p1b = 0;
   int segs2 = 0;
   if (x_end2 > x_begin2) {   // second range, same segment length and rows per block
@@ -718,15 +723,20 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
     a.p1b = x_end2 - s.xl0;
     segs2 = (a.p1b - a.p0b + a.sx - 1) / a.sx;
   }
-  const unsigned grid = (unsigned)(a.ntiles_y * (segs + segs2));
+  const unsigned grid = (unsigned)(a.ntiles_y * (segs + segs2) * a.zchunks);
   if (tma) {
     const size_t smem = fused_tma_smem<R>(a.ty, threads);
     if (col) k_step_fused_tma<R, true><<<grid, threads, smem, st>>>(d, a);
     else k_step_fused_tma<R, false><<<grid, threads, smem, st>>>(d, a);
   } else {
     const size_t smem = fused_smem<R>(a.ty, threads);
-    if (col) k_step_fused<R, true><<<grid, threads, smem, st>>>(d, a);
-    else k_step_fused<R, false><<<grid, threads, smem, st>>>(d, a);
+    if (a.zchunks > 1) {
+      if (col) k_step_fused<R, true, true><<<grid, threads, smem, st>>>(d, a);
+      else k_step_fused<R, false, true><<<grid, threads, smem, st>>>(d, a);
+    } else {
+      if (col) k_step_fused<R, true, false><<<grid, threads, smem, st>>>(d, a);
+      else k_step_fused<R, false, false><<<grid, threads, smem, st>>>(d, a);
+    }
   }
   return VX_OK;
 }

@@ -714,6 +714,7 @@ template <class R> struct FusedArgs {
   int p0, p1;       // local planes to update [p0, p1)
   int p0b, p1b;     // a second range, for blocks >= nblk0 (a slab's two boundary planes)
   int nblk0;
+  int zchunks;      // z chunks of blockDim voxels (1 for nz <= 256)
   int ntiles_y;
   int nplanes;      // planes in the local box
 };
@@ -741,7 +742,7 @@ template <class R> __device__ __forceinline__ VS<R> vs_shfl_down(const VS<R>& s)
   return o;
 }
 
-template <class R, bool COLLIDE>
+template <class R, bool COLLIDE, bool ZC>
 __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<R> d, FusedArgs<R> a) {
   using R4 = typename VT<R>::R4;
   using R2 = typename VT<R>::R2;
@@ -755,10 +756,18 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
   Rec6<R>* yrec = reinterpret_cast<Rec6<R>*>(edge + 2 * (nzb / 32));   // thread-private -y slot
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = nzb >> 5;
 
-  const int k = threadIdx.x;
-  const bool act = k < (int)d.nz;
+  // z chunks of blockDim voxels (nz > 256): chunk zc covers k in [kz0, kz0 + nzb)
+  const int tk = threadIdx.x;
   int bid = blockIdx.x, p0 = a.p0, p1 = a.p1;
   if (bid >= a.nblk0) { bid -= a.nblk0; p0 = a.p0b; p1 = a.p1b; }
+  int kz0 = 0;
+  if constexpr (ZC) {   // nz > 256
+    const int zc = bid % a.zchunks;
+    bid /= a.zchunks;
+    kz0 = zc * nzb;
+  }
+  const int k = kz0 + tk;
+  const bool act = k < (int)d.nz;
   const int tile = bid % a.ntiles_y;
   const int seg = bid / a.ntiles_y;
   const int j0 = tile * a.ty;
@@ -786,12 +795,12 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
           r = rec6(Fa, Mb);
         }
       }
-      xrec[(size_t)(j - j0) * nzb + k] = r;
+      xrec[(size_t)(j - j0) * nzb + tk] = r;
     }
 
   for (int i = i0; i < i1; ++i) {
     VS<R> va, vb;    // ping-pong: this row's voxel and the next row's
-    Rec6<R>& ry = yrec[k];   // -y slot record of the current row: +y bond of the row below
+    Rec6<R>& ry = yrec[tk];   // -y slot record of the current row: +y bond of the row below
     ry = Rec6<R>{};
     if (act) {
       va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0));
@@ -832,8 +841,8 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
         }
       }
       VS<R> vz = vs_shfl_down(cur);
-      if (lane == 31 && (meta & nb_bit(5))) {
-        if (j > j0) vz = edge[(par ^ 1) * nwarp + warp + 1];
+      if (lane == 31 && (meta & nb_bit(5))) {   // the last lane of the block: the next chunk's
+        if (j > j0 && (!ZC || warp + 1 < nwarp)) vz = edge[(par ^ 1) * nwarp + warp + 1];
         else vz = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + 1);
       }
       V3<R> FX{}, MX{}, BX{}, FY{}, MY{}, BY{}, FZ{}, MZ{}, BZ{};
@@ -847,9 +856,19 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
       }
       if (lane == 0 && warp > 0 && (FULL || act) && j + 1 < j1) edge[par * nwarp + warp] = nxt;
       Rec6<R>* zr = zrec + (size_t)par * nzb;
-      if (FULL || act) zr[k] = rec6(FZ, BZ);
+      if (FULL || act) zr[tk] = rec6(FZ, BZ);
+      // the first lane of a later z chunk: its -z bond belongs to the chunk below,
+      // recomputed here (halo)
+      Rec6<R> zlo{};
+      if (ZC && tk == 0 && kz0 > 0 && (meta & nb_bit(4))) {
+        const VS<R> vl = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id - 1);
+        const AFrame<R> f = a_frame(d, vl);
+        V3<R> Fa, Ma, Mb;
+        bond_eval<2>(d, f.Ra, vl.q, f.ua, f.Va, f.wa, f.mat, cur, dT, Fa, Ma, Mb);
+        zlo = rec6(Fa, Mb);
+      }
       // K4's slot order -x, +x, -y, +y | -z, +z: the first four before the barrier
-      Rec6<R>& xr = xrec[(size_t)(j - j0) * nzb + k];
+      Rec6<R>& xr = xrec[(size_t)(j - j0) * nzb + tk];
       V3<R> F = mk(R(0), R(0), R(0)), M = F;
       if (FULL || (meta & nb_bit(0))) slot_minus(F, M, xr);
       if (FULL || (meta & nb_bit(1))) slot_plus(F, M, FX, MX);
@@ -860,10 +879,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
       __syncthreads();
       if (!FULL && !act) return;
       if (FULL || (meta & (M_FILLED | M_FIXED)) == M_FILLED) {
-        if (meta & nb_bit(4)) {
-          const Rec6<R>& z = zr[k - 1];
-          slot_minus(F, M, z);
-        }
+        if (meta & nb_bit(4)) slot_minus(F, M, (!ZC || tk > 0) ? zr[tk - 1] : zlo);
         if (meta & nb_bit(5)) slot_plus(F, M, FZ, MZ);
         const R v = finish_voxel<R, COLLIDE>(d, id, k, cur, meta, F, M, a.opos, a.oquat, a.omom,
                                              a.oang, a.ext_of_local);

@@ -7,7 +7,7 @@ import pytest
 
 import workloads as W
 from parity import errors, oracle_for
-from paper_1212_2845_b200 import VoxError, from_scene
+from paper_1212_2845_b200 import from_scene
 
 pytestmark = pytest.mark.gpu
 
@@ -103,9 +103,21 @@ def test_fused_engine_switch_and_checkpoint():
     assert d <= 1e-5 * np.abs(a.read_state().pos - sc.initial_state()[0]).max()
 
 
-def test_fused_rejects_tall_z():
-    sc = W.Scene("tall", np.ones((300, 1, 2), np.uint8), 1e-3, [dict(E=1e6, nu=0.35, rho=1000.0)],
-                 W._env())
-    lat = from_scene(sc, precision=32)
-    with pytest.raises(VoxError):
-        lat.set_engine("fused")
+@pytest.mark.parametrize("prec", [64, 32])
+def test_fused_tall_z_chunks_match_oracle(prec):
+    """nz > 256: the sweep runs z chunks of 256 (each chunk's lowest lane
+    recomputes its -z bond); two-material column on the floor under gravity."""
+    nz = 300
+    cells = np.ones((nz, 2, 3), np.uint8)
+    cells[nz // 2:] = 2
+    sc = W.Scene("tall", cells, 1e-3, [dict(E=1e6, nu=0.35, rho=1000.0, mu_s=0.5, mu_d=0.5),
+                                      dict(E=5e6, nu=0.35, rho=1200.0, mu_s=0.5, mu_d=0.5)],
+                 W._env(gravity=9.81, floor_on=1, zeta_bond=1.0))
+    lat = from_scene(sc, precision=prec, engine="fused")
+    assert lat.engine == "fused"
+    o = oracle_for(sc)
+    lat.step(100)
+    o.step(100)
+    g, r = lat.read_state(), o.read_state()
+    e = errors(g, r, sc.initial_state()[0], sc.lattice_dim)
+    assert e["eD"] <= {64: 1e-9, 32: 1e-4}[prec], e

@@ -45,12 +45,17 @@ def _scenes():
     b.env["zeta_ground"] = 0.0
     w = W.walker(24, 12, 40)
     w.env["T_freq"] = 1000.0
+    cells = np.ones((300, 5, 6), np.uint8)          # nz > 256: two z chunks
+    cells[150:] = 2
+    tall = W.Scene("tall", cells, 1e-3, [dict(E=1e6, nu=0.35, rho=1000.0, mu_s=0.5, mu_d=0.5),
+                                        dict(E=5e6, nu=0.35, rho=1200.0, mu_s=0.5, mu_d=0.5)],
+                   W._env(gravity=9.81, floor_on=1, zeta_bond=1.0))
     return {"block": (b, 60), "walker": (w, 60), "C2c": (W.get("C2c"), 120),
-            "sphere": (W.hollow_sphere(n=14, r_in=4, r_out=7), 200)}
+            "sphere": (W.hollow_sphere(n=14, r_in=4, r_out=7), 200), "tall": (tall, 80)}
 
 
 @pytest.mark.parametrize("prec", [32, 64])
-@pytest.mark.parametrize("name", ["block", "walker", "C2c", "sphere"])
+@pytest.mark.parametrize("name", ["block", "walker", "C2c", "sphere", "tall"])
 def test_geometry_bitwise(name, prec):
     sc, steps = _scenes()[name]
     ref = _run(sc, prec, steps)
