@@ -43,11 +43,11 @@ ALG_BYTES = {
     32: {"bonds": 56 + 108, "integrate": 108 + 56 + 56, "fused": 56 + 56},
     64: {"bonds": 112 + 216, "integrate": 216 + 112 + 112, "fused": 112 + 112},
 }
-# Issue side of the fused kernel, counted by ncu on C5 fp32 at the tuned geometry TY=7, SX=32 (profiles/r09_geometry.md):
+# Issue side of the fused kernel, counted by ncu on C5 fp32 at the tuned geometry TY=7, SX=32 (profiles/r09_geometry.md, r11):
 # issue slots per voxel-step (smsp__inst_executed / voxels), FP32 lane-operations
 # (scalar FADD/FMUL/FFMA thread-instructions + 2 x the packed FADD2/FMUL2/FFMA2
 # ones) and FLOP (an FMA lane-op = 2) per voxel-step.
-FUSED_COUNTS = {32: {"warp_inst": 876033032 / 33554432, "fp32_ops": 587.1, "flop": 891.4}}
+FUSED_COUNTS = {32: {"warp_inst": 883452624 / 33554432, "fp32_ops": 587.1, "flop": 891.4}}
 
 
 def alu_roof(prec, ms, voxels, clocks):
