@@ -93,6 +93,7 @@ struct Slab {
   DevBuf buf[2][4];                    // state, double-buffered: [parity][pos, quat, mom, ang]
   int par = 0;                         // which copy holds the current state S_n
   DevBuf recA, recB, recC, fextd, cf, meta_d, ext_of_local;
+  DevBuf sidx;                            // global surface index per local voxel (collision)
   std::vector<uint32_t> meta_static;   // static meta bits, local box order
   DevBuf& pos() { return buf[par][0]; }
   DevBuf& quat() { return buf[par][1]; }
@@ -145,6 +146,7 @@ struct vx_lattice {
   DevBuf surf_d, ss, cellh, bcount, bstart, bitems, rowptr, col;
   int H = 0;
   int bp_grid = 1;                        // CTAs of the cooperative broadphase
+  bool ss_dirty = true;                   // the surface table must be re-packed from the state
   long long cap = 0;
   double cutoff = 0;
   // staging of the external fp64 state (vx_set_state / vx_read_state), kept between calls
@@ -199,7 +201,7 @@ struct vx_lattice {
     return k;
   }
   // clock + (surface pack and contact per slab + broadphase when colliding)
-  int other_launches() const { return 1 + (collide() ? 1 + 2 * (int)slabs.size() : 0); }
+  int other_launches() const { return 1 + (collide() ? 1 + (int)slabs.size() : 0); }
   int launches_per_step() const {
     int k = 1;                                         // clock
     k += fused() ? fused_launches() : bond_launches() + (int)slabs.size();
@@ -291,6 +293,8 @@ template <class R> Dev<R> make_dev(const vx_lattice* h, const Slab& s) {
   d.recC = s.recC.as<R>();
   d.fext = h->any_ext ? s.fextd.as<typename VT<R>::R4>() : nullptr;
   d.cf = s.cf.as<typename VT<R>::R4>();
+  d.sidx = s.sidx.as<int>();
+  d.ss = h->ss.as<typename VT<R>::R4>();
   d.mat = h->mat.as<MatC<R>>();
   d.pair = h->pair.as<PairC<R>>();
   d.clk = h->clk.as<Clock>();
@@ -509,10 +513,17 @@ vx_status setup_collision(vx_lattice* h) {
   VX_TRY(h->rowptr.alloc((size_t)(S + 1) * 4));
   VX_TRY(h->col.alloc((size_t)h->cap * 4));
   VX_CUDA(cudaMemset(h->rowptr.p, 0, (size_t)(S + 1) * 4));
-  for (Slab& sl : h->slabs) {
+  for (size_t q = 0; q < h->slabs.size(); ++q) {
+    Slab& sl = h->slabs[q];
     VX_TRY(sl.cf.alloc((size_t)sl.nloc * 4 * r));
     VX_CUDA(cudaMemset(sl.cf.p, 0, sl.cf.bytes));
+    std::vector<int> si(sl.nloc, -1);
+    for (int s = h->slab_seg(q, 0); s < h->slab_seg(q, 1); ++s)
+      si[(size_t)((long long)h->surf_g[s] - sl.box_base)] = s;
+    VX_TRY(sl.sidx.alloc((size_t)sl.nloc * 4));
+    VX_CUDA(cudaMemcpy(sl.sidx.p, si.data(), (size_t)sl.nloc * 4, cudaMemcpyHostToDevice));
   }
+  h->ss_dirty = true;
   // cutoff = 2 r_max + horizon, r_max = (l/2)(1 + max|alpha| |T_amp|)
   double amax = 0;
   for (auto& m : h->mats) amax = std::max(amax, std::fabs(m.cte));
@@ -654,6 +665,7 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   VX_CUDA(cudaMemcpy(h->clk.p, &saved, sizeof saved, cudaMemcpyHostToDevice));
+  h->ss_dirty = true;   // the candidates wrote S_{n+1} entries into the surface table
   if (h->geo_tuned.empty()) h->geo_tuned[-1] = {0, 0};   // nothing to tune: do not retry
   h->clear_graphs();
   return VX_OK;
@@ -825,11 +837,8 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
     using R4 = typename VT<R>::R4;
     R4* ss = h->ss.as<R4>();
     const unsigned* gb = h->surf_d.as<unsigned>();
-    for (size_t q = 0; q < h->slabs.size(); ++q) {
-      const int s0 = h->slab_seg(q, 0), s1 = h->slab_seg(q, 1);
-      if (s1 > s0)
-        k_surf_pack<R><<<grid_of(s1 - s0), 256, 0, h->stream>>>(make_dev<R>(h, h->slabs[q]), gb, s0, s1, ss);
-    }
+    // each slab's segment of the table was written by the previous step's update
+    // (surface_entry) or by pack_surface after a state change
     if (h->nccl()) {   // every rank's segment of the surface table to every rank
       VX_NCCL(ncclGroupStart());
       for (int r = 0; r < h->nranks; ++r) {
@@ -919,8 +928,23 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
   return VX_OK;
 }
 
+template <class R> vx_status pack_surface(vx_lattice* h) {
+  using R4 = typename VT<R>::R4;
+  for (size_t q = 0; q < h->slabs.size(); ++q) {
+    const int s0 = h->slab_seg(q, 0), s1 = h->slab_seg(q, 1);
+    if (s1 > s0)
+      k_surf_pack<R><<<grid_of(s1 - s0), 256, 0, h->stream>>>(make_dev<R>(h, h->slabs[q]),
+                                                               h->surf_d.as<unsigned>(), s0, s1,
+                                                               h->ss.as<R4>());
+  }
+  VX_CUDA(cudaGetLastError());
+  h->ss_dirty = false;
+  return VX_OK;
+}
+
 template <class R> vx_status run_steps(vx_lattice* h, long long n) {
   VX_TRY(tune_fused<R>(h));
+  if (h->collide() && h->ss_dirty) VX_TRY(pack_surface<R>(h));
   // CUDA graphs of G steps; the remainder is captured as its own graph.  The
   // fused engine ping-pongs two state copies, so a graph also depends on which
   // copy is current when it starts (key = 2 g + parity).  With instrumentation
@@ -1330,6 +1354,7 @@ vx_status vx_set_state(vx_lattice* h, const double* pos, const double* quat, con
     VX_CUDA(cudaGetLastError());
   }
   VX_CUDA(cudaStreamSynchronize(h->stream));
+  h->ss_dirty = true;
   return set_force_rebuild(h);
 }
 
@@ -1393,6 +1418,7 @@ vx_status vx_load_checkpoint(vx_lattice* h, const void* buf, int64_t bytes) {
   c.overflow = 0;
   VX_CUDA(cudaMemcpy(h->clk.p, &c, sizeof c, cudaMemcpyHostToDevice));
   h->steps_done = hd.steps_done;
+  h->ss_dirty = true;
   // static meta bits follow this lattice's boundary conditions (latch kept)
   return upload_meta(h);
 }

@@ -47,6 +47,8 @@ template <class R> struct Dev {
   R* recC;    // [3][nloc]
   const R4* fext;
   R4* cf;     // contact force per voxel (collision only)
+  const int* sidx;   // global surface index of an owned surface voxel, else -1 (collision)
+  R4* ss;            // surface table (collision): ss[2s] = pos, ss[2s+1] = mom of S_n
   const MatC<R>* mat;
   const PairC<R>* pair;
   Clock* clk;
@@ -427,6 +429,19 @@ template <class R> __device__ __forceinline__ void flag_nonfinite(const Dev<R>& 
     atomicMin(&d.clk->err, code);
   }
 }
+// A surface voxel's new state also goes to the surface table, so the next
+// step's contact front reads it without a separate pack (k_surf_pack only
+// initialises the table after a state change).
+template <class R>
+__device__ __forceinline__ void surface_entry(const Dev<R>& d, uint32_t id, uint32_t nmeta,
+                                              const typename VT<R>::R4& npos,
+                                              const typename VT<R>::R4& nmom) {
+  if (!(nmeta & M_SURF)) return;
+  const int s = d.sidx[id];
+  if (s < 0) return;
+  d.ss[2 * s] = npos;
+  d.ss[2 * s + 1] = nmom;
+}
 template <class R, bool COLLIDE>
 __device__ __forceinline__ R integrate_store(const Dev<R>& d, uint32_t id, const VS<R>& s,
                                              uint32_t nmeta, const MatC<R>& mc, V3<R> F, V3<R> M,
@@ -454,10 +469,12 @@ __device__ __forceinline__ R integrate_store(const Dev<R>& d, uint32_t id, const
   R qz = dw * q.z + dx * q.y - dy * q.x + dz * q.w;
   const R qi = vx_rnorm(qw * qw + qx * qx + qy * qy + qz * qz);
   qw = qw * qi; qx = qx * qi; qy = qy * qi; qz = qz * qi;
-  st_stream(opos + id, R4{u.x, u.y, u.z, meta_as(R(0), nmeta)});
+  const R4 npos{u.x, u.y, u.z, meta_as(R(0), nmeta)}, nmom{P.x, P.y, P.z, phi.z};
+  st_stream(opos + id, npos);
   st_stream(oquat + id, R4{qx, qy, qz, qw});
-  st_stream(omom + id, R4{P.x, P.y, P.z, phi.z});
+  st_stream(omom + id, nmom);
   st_stream(oang + id, R2{phi.x, phi.y});
+  if constexpr (COLLIDE) surface_entry(d, id, nmeta, npos, nmom);
   // any NaN/Inf among the 13 values: x * 0 is NaN exactly for non-finite x
   const R z0 = (u.x + u.y + u.z + qw + qx + qy + qz) * R(0);
   const R z1 = (P.x + P.y + P.z + phi.x + phi.y + phi.z) * R(0);
@@ -499,10 +516,13 @@ __device__ __forceinline__ float integrate_store_f32(const Dev<float>& d, uint32
   const float qi = vx_rnorm(f2lo(nn) + f2hi(nn));
   q1 = mul2(bc2(qi), q1);
   q2 = mul2(bc2(qi), q2);
-  st_stream(opos + id, float4{f2lo(uxy), f2hi(uxy), uz, meta_as(0.f, nmeta)});
+  const float4 npos{f2lo(uxy), f2hi(uxy), uz, meta_as(0.f, nmeta)};
+  const float4 nmom{f2lo(Pxy), f2hi(Pxy), Pz, phz};
+  st_stream(opos + id, npos);
   st_stream(oquat + id, float4{f2lo(q1), f2hi(q1), f2lo(q2), f2hi(q2)});
-  st_stream(omom + id, float4{f2lo(Pxy), f2hi(Pxy), Pz, phz});
+  st_stream(omom + id, nmom);
   st_stream(oang + id, float2{f2lo(phxy), f2hi(phxy)});
+  if constexpr (COLLIDE) surface_entry(d, id, nmeta, npos, nmom);
   // any NaN/Inf among the 13 values: x * 0 is NaN exactly for non-finite x
   const f2_t sxy = add2(add2(add2(add2(uxy, q1), q2), Pxy), phxy);
   flag_nonfinite(d, id, (f2lo(sxy) + f2hi(sxy) + uz + Pz + phz) * 0.f, ext_of_local);
