@@ -600,9 +600,13 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
   const bool col = h->collide();
   Clock saved;   // the candidates' motion-budget / divergence atomics must not leak
   VX_CUDA(cudaMemcpy(&saved, h->clk.p, sizeof saved, cudaMemcpyDeviceToHost));
-  cudaEvent_t e0, e1;
-  VX_CUDA(cudaEventCreate(&e0));
-  VX_CUDA(cudaEventCreate(&e1));
+  struct Ev {   // released on every exit path
+    cudaEvent_t e = nullptr;
+    ~Ev() { if (e) cudaEventDestroy(e); }
+  } ev0, ev1;
+  VX_CUDA(cudaEventCreate(&ev0.e));
+  VX_CUDA(cudaEventCreate(&ev1.e));
+  const cudaEvent_t e0 = ev0.e, e1 = ev1.e;
   for (const Slab& s : h->slabs) {
     const int b = split ? s.x0 + 1 : s.x0, e = split ? s.x1 - 1 : s.x1;
     const int planes = e - b;
@@ -662,8 +666,6 @@ template <class R> vx_status tune_fused(vx_lattice* h) {
       std::fprintf(stderr, "voxsim: fused geometry for planes [%d, %d): TY=%d SX=%d (%.3f ms / launch)\n", b, e,
                    best_g.first, best_g.second, best_t);
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   VX_CUDA(cudaMemcpy(h->clk.p, &saved, sizeof saved, cudaMemcpyHostToDevice));
   h->ss_dirty = true;   // the candidates wrote S_{n+1} entries into the surface table
   if (h->geo_tuned.empty()) h->geo_tuned[-1] = {0, 0};   // nothing to tune: do not retry
