@@ -1,0 +1,56 @@
+"""Randomised small scenes (seeded): irregular occupancy, odd shapes, fixed and
+forced voxels, floor / gravity / temperature / self collision on or off --
+the CUDA path (both engines, fp64) against the oracle after 150 steps, and the
+fp32 fused path within the fp32 bar.  Catches edge cases the named configs
+do not reach."""
+import numpy as np
+import pytest
+
+import workloads as W
+from parity import errors, run_pair
+
+pytestmark = pytest.mark.gpu
+
+
+def _scene(seed):
+    rng = np.random.default_rng(1000 + seed)
+    nx, ny, nz = (int(v) for v in rng.integers(1, 14, size=3))
+    nz = int(rng.choice([nz, 33, 40])) if seed % 3 == 0 else nz
+    fill = rng.uniform(0.35, 1.0)
+    cells = (rng.random((nz, ny, nx)) < fill).astype(np.uint8)
+    nm = int(rng.integers(1, 4))
+    cells *= rng.integers(1, nm + 1, size=cells.shape).astype(np.uint8)
+    if cells.sum() == 0:
+        cells[0, 0, 0] = 1
+    mats = [dict(E=float(10 ** rng.uniform(5.5, 7)), nu=float(rng.uniform(0.2, 0.45)),
+                 rho=float(rng.uniform(800, 1600)), cte=float(rng.uniform(-0.005, 0.005)),
+                 mu_s=0.6, mu_d=0.4) for _ in range(nm)]
+    floor = bool(rng.random() < 0.6)
+    env = W._env(gravity=9.81 if rng.random() < 0.7 else 0.0, floor_on=int(floor),
+                 zeta_bond=float(rng.uniform(0.2, 0.9)), zeta_ground=float(rng.uniform(0, 0.05)),
+                 zeta_col=0.5, T_amp=float(rng.uniform(0, 5)), T_freq=200.0,
+                 self_collision=int(rng.random() < 0.4), horizon_voxels=1.5)
+    sc = W.Scene(f"fuzz{seed}", cells, 1e-3, mats, env, origin=(0.0, 0.0, 1e-5 if floor else 0.0))
+    n = sc.num_voxels
+    sc.fixed = (rng.random(n) < 0.1).astype(np.uint8)
+    sc.fext = np.where(rng.random((n, 1)) < 0.1, rng.normal(0, 1e-3, (n, 3)), 0.0)
+    sc.v0 = rng.normal(0, 0.05, (n, 3))
+    return sc
+
+
+@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("engine", ["fused", "two_pass"])
+def test_fuzz_fp64(seed, engine):
+    sc = _scene(seed)
+    g, o, p0, lat, orc = run_pair(sc, 150, 64, chunks=3, engine=engine)
+    e = errors(g, o, p0, sc.lattice_dim)
+    assert e["eD"] <= 1e-9, (seed, engine, e, sc.cells.shape)
+    assert np.array_equal(g.latch, o.latch)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_fuzz_fp32_fused(seed):
+    sc = _scene(seed)
+    g, o, p0, lat, orc = run_pair(sc, 150, 32, engine="fused")
+    e = errors(g, o, p0, sc.lattice_dim)
+    assert e["eD"] <= 1e-4, (seed, e, sc.cells.shape)
