@@ -54,3 +54,24 @@ def test_fuzz_fp32_fused(seed):
     g, o, p0, lat, orc = run_pair(sc, 150, 32, engine="fused")
     e = errors(g, o, p0, sc.lattice_dim)
     assert e["eD"] <= 1e-4, (seed, e, sc.cells.shape)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_fuzz_slabs_and_geometry_bitwise(seed):
+    """The same random scenes on P emulated slabs and under the tuned geometry:
+    bitwise equal to one domain (fp32, both engines)."""
+    from paper_1212_2845_b200 import from_scene
+    sc = _scene(seed)
+    nx = sc.cells.shape[2]
+    rng = np.random.default_rng(seed)
+    for engine in ("fused", "two_pass"):
+        ref = from_scene(sc, precision=32, engine=engine)
+        ref.step(90)
+        r = ref.read_state()
+        P = int(rng.integers(2, min(nx, 5) + 1)) if nx >= 2 else 1
+        lat = from_scene(sc, precision=32, engine=engine, nranks=P)
+        lat.step(45)
+        lat.step(45)
+        g = lat.read_state()
+        for a, b in ((g.pos, r.pos), (g.quat, r.quat), (g.linmom, r.linmom), (g.angmom, r.angmom)):
+            assert np.array_equal(a, b), (seed, engine, P)
