@@ -249,7 +249,9 @@ def run_ours(args):
     # millisecond kernels) unless the lattice is small, where CUDA graphs carry the
     # step and the kernel breakdown comes from a separate instrumented pass.
     live = N >= 2_000_000 if args.timing == "auto" else args.timing == "live"
-    lat.set_instrumentation(live)
+    # live: event nodes on every 8th step of the timed region (the kernels'
+    # average launch time, at 1/8 of the event overhead)
+    lat.set_instrumentation(live, stride=8)
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
@@ -262,12 +264,11 @@ def run_ours(args):
     barrier()
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
-    n_instr = args.steps
     if not live:
-        n_instr = min(args.steps, 50)
         lat.set_instrumentation(True)
-        lat.step(n_instr)
+        lat.step(min(args.steps, 50))
     kt = lat.kernel_times()
+    n_instr = max(1, round(kt["all"][1] / max(lat.launches_per_step, 1)))   # measured steps
     lat.set_instrumentation(False)
     ms_max = vd.max_over_ranks([ms], dist if world > 1 else None, "cuda")[0]
     value = N * args.steps / (ms_max / 1e3)

@@ -201,9 +201,10 @@ int64_t vx_contact_pairs(vx_lattice* h, int64_t* pairs, int64_t cap);
  * Owned by the library; valid until vx_destroy. */
 void* vx_stream(const vx_lattice* h);
 
-/* Kernel-level instrumentation.  When on, the CUDA graphs vx_step replays
- * carry CUDA event-record nodes around every launch class of every step (on
- * vx_stream()), read back after each graph replay; vx_kernel_times returns,
+/* Kernel-level instrumentation.  on = 0: off; on = 1: the CUDA graphs vx_step
+ * replays carry CUDA event-record nodes around every launch class of every
+ * step (on vx_stream()); on = n > 1: of every n-th step.  The times of one
+ * graph replay are read while the next one runs; vx_kernel_times returns,
  * since the last reset, the summed device time in ms and the launch count of
  * each kernel class: out_ms[0]/counts[0] = K3 bonds, [1] = K4
  * gather-integrate or the fused pass, [2] = other (clock, surface table,

@@ -155,6 +155,7 @@ struct vx_lattice {
   std::map<long long, cudaGraphExec_t> graphs;
   // instrumentation
   bool instr = false;
+  int instr_stride = 1;                   // events on every instr_stride-th step
   std::vector<cudaEvent_t> events;
   double t_ms[4] = {0, 0, 0, 0};
   long long t_cnt[4] = {0, 0, 0, 0};
@@ -944,6 +945,30 @@ template <class R> vx_status pack_surface(vx_lattice* h) {
   return VX_OK;
 }
 
+// Accumulate the event times of one instrumented graph chunk (events of the
+// measured steps only; pool offset `base`).
+vx_status read_chunk_times(vx_lattice* h, size_t base, long long g) {
+  for (long long s = 0; s < g; s += h->instr_stride) {
+    cudaEvent_t* e = &h->events[base + (size_t)s * 4];
+    VX_CUDA(cudaEventSynchronize(e[3]));
+    float a = 0, b, c, t;
+    if (h->fused()) {
+      VX_CUDA(cudaEventElapsedTime(&c, e[0], e[2]));
+    } else {
+      VX_CUDA(cudaEventElapsedTime(&a, e[1], e[2]));
+      VX_CUDA(cudaEventElapsedTime(&c, e[0], e[1]));
+    }
+    VX_CUDA(cudaEventElapsedTime(&b, e[2], e[3]));
+    VX_CUDA(cudaEventElapsedTime(&t, e[0], e[3]));
+    h->t_ms[0] += a; h->t_ms[1] += b; h->t_ms[2] += c; h->t_ms[3] += t;
+    h->t_cnt[0] += h->fused() ? 0 : h->bond_launches();
+    h->t_cnt[1] += h->fused() ? h->fused_launches() : (long long)h->slabs.size();
+    h->t_cnt[2] += h->other_launches();
+    h->t_cnt[3] += h->launches_per_step();
+  }
+  return VX_OK;
+}
+
 template <class R> vx_status run_steps(vx_lattice* h, long long n) {
   VX_TRY(tune_fused<R>(h));
   if (h->collide() && h->ss_dirty) VX_TRY(pack_surface<R>(h));
@@ -951,27 +976,34 @@ template <class R> vx_status run_steps(vx_lattice* h, long long n) {
   // fused engine ping-pongs two state copies, so a graph also depends on which
   // copy is current when it starts (key = 2 g + parity).  With instrumentation
   // on, the graphs carry event-record nodes around every launch class of every
-  // step (their own cache); the times are read after each graph replay.
+  // instr_stride-th step (their own cache); two event pools alternate between
+  // graph replays, so a chunk's times are read while the next chunk runs.
   const long long G = 32;
   if (h->instr) {
-    while (h->events.size() < (size_t)G * 4) {
+    while (h->events.size() < (size_t)G * 8) {
       cudaEvent_t e;
       VX_CUDA(cudaEventCreate(&e));
       h->events.push_back(e);
     }
   }
   long long left = n;
+  int pool = 0;
+  long long pending = 0;   // steps of the chunk in flight whose times are unread
   while (left > 0) {
     const long long g = left >= G ? G : left;
     const int par = h->slabs[0].par;
-    const long long key = 2 * g + (h->fused() ? par : 0) + (h->instr ? (1LL << 40) : 0);
+    const long long key = 2 * g + (h->fused() ? par : 0) +
+                          (h->instr ? ((long long)h->instr_stride << 40) + ((long long)pool << 39) : 0);
     auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {
       cudaGraph_t graph;
       VX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
       vx_status st = VX_OK;
-      for (long long s = 0; s < g && st == VX_OK; ++s)
-        st = enqueue_step<R>(h, h->instr ? &h->events[(size_t)s * 4] : nullptr);
+      for (long long s = 0; s < g && st == VX_OK; ++s) {
+        cudaEvent_t* ev = nullptr;
+        if (h->instr && s % h->instr_stride == 0) ev = &h->events[(size_t)pool * G * 4 + (size_t)s * 4];
+        st = enqueue_step<R>(h, ev);
+      }
       cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
       for (auto& s : h->slabs) s.par = par;   // capture only recorded the flips
       if (st != VX_OK) return st;
@@ -985,26 +1017,12 @@ template <class R> vx_status run_steps(vx_lattice* h, long long n) {
     if (h->fused() && (g & 1)) h->flip();
     left -= g;
     if (h->instr) {
-      VX_CUDA(cudaStreamSynchronize(h->stream));
-      for (long long s = 0; s < g; ++s) {
-        cudaEvent_t* e = &h->events[(size_t)s * 4];
-        float a = 0, b, c, t;
-        if (h->fused()) {
-          VX_CUDA(cudaEventElapsedTime(&c, e[0], e[2]));
-        } else {
-          VX_CUDA(cudaEventElapsedTime(&a, e[1], e[2]));
-          VX_CUDA(cudaEventElapsedTime(&c, e[0], e[1]));
-        }
-        VX_CUDA(cudaEventElapsedTime(&b, e[2], e[3]));
-        VX_CUDA(cudaEventElapsedTime(&t, e[0], e[3]));
-        h->t_ms[0] += a; h->t_ms[1] += b; h->t_ms[2] += c; h->t_ms[3] += t;
-        h->t_cnt[0] += h->fused() ? 0 : h->bond_launches();
-        h->t_cnt[1] += h->fused() ? h->fused_launches() : (long long)h->slabs.size();
-        h->t_cnt[2] += h->other_launches();
-        h->t_cnt[3] += h->launches_per_step();
-      }
+      if (pending) VX_TRY(read_chunk_times(h, (size_t)(pool ^ 1) * G * 4, pending));
+      pending = g;
+      pool ^= 1;
     }
   }
+  if (h->instr && pending) VX_TRY(read_chunk_times(h, (size_t)(pool ^ 1) * G * 4, pending));
   VX_CUDA(cudaStreamSynchronize(h->stream));
   return VX_OK;
 }
@@ -1632,6 +1650,7 @@ int64_t vx_contact_pairs(vx_lattice* h, int64_t* pairs, int64_t cap) {
 vx_status vx_set_instrumentation(vx_lattice* h, int32_t on) {
   if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
   h->instr = on != 0;
+  h->instr_stride = on > 1 ? on : 1;
   for (int i = 0; i < 4; ++i) { h->t_ms[i] = 0; h->t_cnt[i] = 0; }
   return VX_OK;
 }

@@ -217,8 +217,10 @@ class Lattice:
         """cudaStream_t of the library (wrap with torch.cuda.ExternalStream)."""
         return int(N.load().vx_stream(self._h) or 0)
 
-    def set_instrumentation(self, on=True):
-        _check(N.load().vx_set_instrumentation(self._h, int(bool(on))))
+    def set_instrumentation(self, on=True, stride=1):
+        """Per-launch CUDA-event timing inside the step graphs, on every
+        `stride`-th step (vx_set_instrumentation)."""
+        _check(N.load().vx_set_instrumentation(self._h, int(stride) if on else 0))
 
     def kernel_times(self):
         ms = (ctypes.c_double * 4)()
