@@ -5,6 +5,9 @@
 // Paper: Hiller & Lipson, arXiv:1212.2845.  Readings: DESIGN.md §3.
 #include "voxsim.h"
 #include "vx_kernels.cuh"
+#include "vx_topology.cuh"
+
+#include <cub/device/device_scan.cuh>
 
 #include <nccl.h>
 
@@ -94,7 +97,7 @@ struct Slab {
   int par = 0;                         // which copy holds the current state S_n
   DevBuf recA, recB, recC, fextd, cf, meta_d, ext_of_local;
   DevBuf sidx;                            // global surface index per local voxel (collision)
-  std::vector<uint32_t> meta_static;   // static meta bits, local box order
+  DevBuf meta_static_d;                  // static meta bits, local box order (K1)
   DevBuf& pos() { return buf[par][0]; }
   DevBuf& quat() { return buf[par][1]; }
   DevBuf& mom() { return buf[par][2]; }
@@ -217,61 +220,84 @@ struct vx_lattice {
 
 namespace {
 
-// ---------------------------------------------------------------- L1 builder
+// ---------------------------------------------------------------- L1/K1 builder
+unsigned topo_grid(unsigned long long n) {
+  return (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>((n + 255) / 256, 148ull * 32));
+}
+
+// out[i] = sum of in[0..i) (cub::DeviceScan, setup only)
+vx_status exclusive_scan_u32(const uint32_t* in, uint32_t* out, unsigned long long n, cudaStream_t st) {
+  size_t tmp = 0;
+  VX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int64_t)n, st));
+  DevBuf t;
+  VX_TRY(t.alloc(std::max<size_t>(tmp, 16)));
+  VX_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, (int64_t)n, st));
+  return VX_OK;
+}
+
+// External ids, static meta of every slab, counts, material-pair table and
+// the surface list, built on the device from the grid (vx_topology.cuh).
 vx_status build_topology(vx_lattice* h) {
   const int nx = h->nx, ny = h->ny, nz = h->nz;
-  auto cell = [&](int i, int j, int k) -> int {
-    if (i < 0 || j < 0 || k < 0 || i >= nx || j >= ny || k >= nz) return 0;
-    return h->cells[(size_t)i + (size_t)nx * ((size_t)j + (size_t)ny * k)];
-  };
+  const unsigned long long nbox = (unsigned long long)h->nbox;
+  cudaStream_t st = h->stream;
+  DevBuf cells_d, flag, scan, counts, pairs, maxc;
+  VX_TRY(cells_d.alloc(nbox));
+  VX_CUDA(cudaMemcpyAsync(cells_d.p, h->cells.data(), nbox, cudaMemcpyHostToDevice, st));
+  VX_TRY(flag.alloc(nbox * 4));
+  VX_TRY(scan.alloc(nbox * 4));
+  const uint8_t* cd = cells_d.as<uint8_t>();
   // external ids: filled cells in x-fastest order (vx_lattice_desc.cells)
-  h->box_of_ext.clear();
-  h->max_cell = 0;
-  for (int k = 0; k < nz; ++k)
-    for (int j = 0; j < ny; ++j)
-      for (int i = 0; i < nx; ++i) {
-        int c = h->cells[(size_t)i + (size_t)nx * ((size_t)j + (size_t)ny * k)];
-        if (!c) continue;
-        h->max_cell = std::max(h->max_cell, c);
-        h->box_of_ext.push_back(((long long)i * ny + j) * nz + k);
-      }
-  h->N = (long long)h->box_of_ext.size();
-  // local box meta: material, filled, neighbour mask, surface
-  for (auto& s : h->slabs) s.meta_static.assign(s.nloc, 0u);
-  h->nbonds = 0;
-  h->nsurf = 0;
-  h->surf_g.clear();
+  k_topo_filled<<<topo_grid(nbox), 256, 0, st>>>(cd, nbox, flag.as<uint32_t>());
+  VX_TRY(exclusive_scan_u32(flag.as<uint32_t>(), scan.as<uint32_t>(), nbox, st));
+  uint32_t last[2] = {0, 0};
+  VX_CUDA(cudaMemcpyAsync(&last[0], scan.as<uint32_t>() + (nbox - 1), 4, cudaMemcpyDeviceToHost, st));
+  VX_CUDA(cudaMemcpyAsync(&last[1], flag.as<uint32_t>() + (nbox - 1), 4, cudaMemcpyDeviceToHost, st));
+  VX_CUDA(cudaStreamSynchronize(st));
+  h->N = (long long)last[0] + last[1];
+  VX_TRY(h->box_of_ext_d.alloc((size_t)std::max<long long>(h->N, 1) * 8));
+  k_topo_ext<<<topo_grid(nbox), 256, 0, st>>>(cd, nx, ny, nz, nbox, scan.as<uint32_t>(),
+                                              h->box_of_ext_d.as<long long>());
+  h->box_of_ext.resize((size_t)h->N);
+  if (h->N)
+    VX_CUDA(cudaMemcpyAsync(h->box_of_ext.data(), h->box_of_ext_d.p, (size_t)h->N * 8, cudaMemcpyDeviceToHost, st));
+  // counts, pair table, surface flags (reusing `flag`)
+  VX_TRY(counts.alloc(16));
+  VX_TRY(pairs.alloc(2048 * 4));
+  VX_TRY(maxc.alloc(4));
+  VX_CUDA(cudaMemsetAsync(counts.p, 0, 16, st));
+  VX_CUDA(cudaMemsetAsync(pairs.p, 0, 2048 * 4, st));
+  VX_CUDA(cudaMemsetAsync(maxc.p, 0, 4, st));
+  k_topo_count<<<topo_grid(nbox), 256, 0, st>>>(cd, nx, ny, nz, nbox, counts.as<unsigned long long>(),
+                                                pairs.as<unsigned>(), maxc.as<int>(), flag.as<uint32_t>());
+  VX_TRY(exclusive_scan_u32(flag.as<uint32_t>(), scan.as<uint32_t>(), nbox, st));
+  unsigned long long cnt[2];
+  std::vector<unsigned> pb(2048);
+  VX_CUDA(cudaMemcpyAsync(cnt, counts.p, 16, cudaMemcpyDeviceToHost, st));
+  VX_CUDA(cudaMemcpyAsync(pb.data(), pairs.p, 2048 * 4, cudaMemcpyDeviceToHost, st));
+  VX_CUDA(cudaMemcpyAsync(&h->max_cell, maxc.p, 4, cudaMemcpyDeviceToHost, st));
+  VX_CUDA(cudaStreamSynchronize(st));
+  h->nbonds = (long long)cnt[0];
+  h->nsurf = (long long)cnt[1];
   h->pair_present.assign(256 * 256, 0);
-  const int di[6] = {-1, 1, 0, 0, 0, 0}, dj[6] = {0, 0, -1, 1, 0, 0}, dk[6] = {0, 0, 0, 0, -1, 1};
-  for (int i = 0; i < nx; ++i)
-    for (int j = 0; j < ny; ++j)
-      for (int k = 0; k < nz; ++k) {
-        const int c = cell(i, j, k);
-        if (!c) continue;
-        uint32_t m = (uint32_t)(c - 1) | M_FILLED;
-        int cnt = 0;
-        for (int s = 0; s < 6; ++s) {
-          const int cb = cell(i + di[s], j + dj[s], k + dk[s]);
-          if (cb) {
-            m |= nb_bit(s);
-            ++cnt;
-            if (s & 1) {
-              ++h->nbonds;
-              h->pair_present[(size_t)(c - 1) * 256 + (cb - 1)] = 1;
-            }
-          }
-        }
-        if (cnt < 6) {
-          m |= M_SURF;
-          ++h->nsurf;
-          h->surf_g.push_back((unsigned)(((long long)i * ny + j) * nz + k));
-        }
-        for (auto& s : h->slabs) {
-          if (i < s.xl0 || i >= s.xl1) continue;
-          const uint32_t li = (uint32_t)(((long long)(i - s.xl0) * ny + j) * nz + k);
-          s.meta_static[li] = m;
-        }
-      }
+  for (int x = 0; x < 65536; ++x)
+    if (pb[x >> 5] & (1u << (x & 31))) h->pair_present[x] = 1;
+  // surface list (global box ids, ascending)
+  h->surf_g.resize((size_t)h->nsurf);
+  if (h->nsurf) {
+    DevBuf sg;
+    VX_TRY(sg.alloc((size_t)h->nsurf * 4));
+    k_topo_surf<<<topo_grid(nbox), 256, 0, st>>>(flag.as<uint32_t>(), scan.as<uint32_t>(), nbox, sg.as<unsigned>());
+    VX_CUDA(cudaMemcpyAsync(h->surf_g.data(), sg.p, (size_t)h->nsurf * 4, cudaMemcpyDeviceToHost, st));
+    VX_CUDA(cudaStreamSynchronize(st));
+  }
+  // static meta of every slab's local box: material, filled, neighbour mask, surface
+  for (auto& s : h->slabs) {
+    VX_TRY(s.meta_static_d.alloc((size_t)s.nloc * 4));
+    k_topo_meta<<<grid_of(s.nloc), 256, 0, st>>>(cd, nx, ny, nz, s.xl0, s.nloc, s.meta_static_d.as<uint32_t>());
+  }
+  VX_CUDA(cudaGetLastError());
+  VX_CUDA(cudaStreamSynchronize(st));
   // surface segment of every rank's slab (box order is x-slowest)
   h->seg.assign((size_t)h->nranks + 1, 0);
   for (int r = 0; r < h->nranks; ++r) {
@@ -316,36 +342,39 @@ template <class R> Dev<R> make_dev(const vx_lattice* h, const Slab& s) {
 }
 
 vx_status upload_meta(vx_lattice* h) {
-  // static bits + boundary bits -> device, merged with the latch bits
+  // static bits + boundary bits (FIXED, EXT) -> device, merged with the latch bits
+  const bool any_fixed = std::any_of(h->fixed.begin(), h->fixed.end(), [](uint8_t v) { return v != 0; });
+  DevBuf fx, fe;
+  if (any_fixed) {
+    VX_TRY(fx.alloc((size_t)h->N));
+    VX_CUDA(cudaMemcpyAsync(fx.p, h->fixed.data(), (size_t)h->N, cudaMemcpyHostToDevice, h->stream));
+  }
+  if (h->any_ext) {
+    VX_TRY(fe.alloc((size_t)h->N * 24));
+    VX_CUDA(cudaMemcpyAsync(fe.p, h->fext.data(), (size_t)h->N * 24, cudaMemcpyHostToDevice, h->stream));
+  }
   for (auto& s : h->slabs) {
-    std::vector<uint32_t> m(s.meta_static);
-    std::vector<double> f4;
-    if (h->any_ext) f4.assign((size_t)s.nloc * 4, 0.0);
-    for (long long e = 0; e < h->N; ++e) {
-      const long long li = h->box_of_ext[e] - s.box_base;
-      if (li < 0 || li >= (long long)s.nloc) continue;
-      m[li] &= ~(M_FIXED | M_EXT);
-      if (!h->fixed.empty() && h->fixed[e]) m[li] |= M_FIXED;
-      if (h->any_ext && (h->fext[3 * e] != 0 || h->fext[3 * e + 1] != 0 || h->fext[3 * e + 2] != 0)) {
-        m[li] |= M_EXT;
-        for (int c = 0; c < 3; ++c) f4[4 * li + c] = h->fext[3 * e + c];
-      }
+    VX_CUDA(cudaMemcpyAsync(s.meta_d.p, s.meta_static_d.p, (size_t)s.nloc * 4, cudaMemcpyDeviceToDevice, h->stream));
+    if (h->any_ext) {
+      VX_TRY(s.fextd.alloc((size_t)s.nloc * 4 * rsize(h->prec)));
+      VX_CUDA(cudaMemsetAsync(s.fextd.p, 0, s.fextd.bytes, h->stream));
     }
-    VX_CUDA(cudaMemcpy(s.meta_d.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice));
+    if ((any_fixed || h->any_ext) && h->N) {
+      const unsigned g = topo_grid((unsigned long long)h->N);
+      if (h->prec == 32)
+        k_apply_bc<float><<<g, 256, 0, h->stream>>>(h->box_of_ext_d.as<long long>(), h->N, s.box_base, s.nloc,
+                                                    fx.as<uint8_t>(), fe.as<double>(), s.meta_d.as<uint32_t>(),
+                                                    s.fextd.as<float4>());
+      else
+        k_apply_bc<double><<<g, 256, 0, h->stream>>>(h->box_of_ext_d.as<long long>(), h->N, s.box_base, s.nloc,
+                                                     fx.as<uint8_t>(), fe.as<double>(), s.meta_d.as<uint32_t>(),
+                                                     s.fextd.as<double4>());
+    }
     if (h->prec == 32)
       k_merge_meta<float><<<grid_of(s.nloc), 256, 0, h->stream>>>(make_dev<float>(h, s), s.meta_d.as<uint32_t>(), s.nloc);
     else
       k_merge_meta<double><<<grid_of(s.nloc), 256, 0, h->stream>>>(make_dev<double>(h, s), s.meta_d.as<uint32_t>(), s.nloc);
     VX_CUDA(cudaGetLastError());
-    if (h->any_ext) {
-      VX_TRY(s.fextd.alloc((size_t)s.nloc * 4 * rsize(h->prec)));
-      if (h->prec == 32) {
-        std::vector<float> f(f4.begin(), f4.end());
-        VX_CUDA(cudaMemcpy(s.fextd.p, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
-      } else {
-        VX_CUDA(cudaMemcpy(s.fextd.p, f4.data(), f4.size() * 8, cudaMemcpyHostToDevice));
-      }
-    }
   }
   VX_CUDA(cudaStreamSynchronize(h->stream));
   h->clear_graphs();
@@ -1185,39 +1214,37 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
     return bail(fail(VX_ERR_CUDA, "stream/event creation failed"));
   if ((s = build_topology(h)) != VX_OK) return bail(s);
   const size_t r = rsize(h->prec);
-  if ((s = h->clk.alloc(sizeof(Clock))) ||
-      (s = h->box_of_ext_d.alloc((size_t)std::max<long long>(h->N, 1) * 8)))
-    return bail(s);
+  if ((s = h->clk.alloc(sizeof(Clock)))) return bail(s);
   for (Slab& sl : h->slabs) {
     const size_t n = sl.nloc;
     if ((s = sl.pos().alloc(n * 4 * r)) || (s = sl.quat().alloc(n * 4 * r)) || (s = sl.mom().alloc(n * 4 * r)) ||
         (s = sl.ang().alloc(n * 2 * r)) ||
         (s = sl.meta_d.alloc(n * 4)) || (s = sl.ext_of_local.alloc(n * 4)))
       return bail(s);
-    // initial state: at rest on the lattice sites, identity orientation (.w = 1)
-    if (cudaMemset(sl.pos().p, 0, sl.pos().bytes) != cudaSuccess || cudaMemset(sl.mom().p, 0, sl.mom().bytes) != cudaSuccess ||
-        cudaMemset(sl.ang().p, 0, sl.ang().bytes) != cudaSuccess)
+    // initial state: at rest on the lattice sites, identity orientation (.w = 1);
+    // external id of every local box (0xffffffff: empty)
+    cudaStream_t st = h->stream;
+    if (cudaMemsetAsync(sl.pos().p, 0, sl.pos().bytes, st) != cudaSuccess ||
+        cudaMemsetAsync(sl.mom().p, 0, sl.mom().bytes, st) != cudaSuccess ||
+        cudaMemsetAsync(sl.ang().p, 0, sl.ang().bytes, st) != cudaSuccess ||
+        cudaMemsetAsync(sl.ext_of_local.p, 0xff, n * 4, st) != cudaSuccess)
       return bail(fail(VX_ERR_CUDA, "memset failed"));
-    std::vector<char> q(sl.quat().bytes, 0);
-    for (size_t i = 0; i < n; ++i) {
-      if (r == 4) { float one = 1.f; std::memcpy(&q[i * 16 + 12], &one, 4); }
-      else { double one = 1.0; std::memcpy(&q[i * 32 + 24], &one, 8); }
-    }
-    std::vector<uint32_t> eol(n, 0xffffffffu);
-    for (long long e = 0; e < h->N; ++e) {
-      const long long li = h->box_of_ext[e] - sl.box_base;
-      if (li >= 0 && li < (long long)n) eol[li] = (uint32_t)e;
-    }
-    if (cudaMemcpy(sl.quat().p, q.data(), q.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(sl.ext_of_local.p, eol.data(), n * 4, cudaMemcpyHostToDevice) != cudaSuccess)
-      return bail(fail(VX_ERR_CUDA, "upload failed"));
+    if (r == 4)
+      k_topo_quat_identity<float><<<grid_of((uint32_t)n), 256, 0, st>>>(sl.quat().as<float4>(), (uint32_t)n);
+    else
+      k_topo_quat_identity<double><<<grid_of((uint32_t)n), 256, 0, st>>>(sl.quat().as<double4>(), (uint32_t)n);
+    if (h->N)
+      k_topo_eol<<<topo_grid((unsigned long long)h->N), 256, 0, st>>>(h->box_of_ext_d.as<long long>(), h->N,
+                                                                      sl.box_base, (uint32_t)n,
+                                                                      sl.ext_of_local.as<uint32_t>());
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+      return bail(fail(VX_ERR_CUDA, "state initialisation failed"));
   }
   if ((s = sync_state_copies(h)) != VX_OK) return bail(s);
   Clock c0{};
   c0.err = ~0ULL;
   c0.force_rebuild = 1;
-  if (cudaMemcpy(h->clk.p, &c0, sizeof c0, cudaMemcpyHostToDevice) != cudaSuccess ||
-      (h->N && cudaMemcpy(h->box_of_ext_d.p, h->box_of_ext.data(), (size_t)h->N * 8, cudaMemcpyHostToDevice) != cudaSuccess))
+  if (cudaMemcpy(h->clk.p, &c0, sizeof c0, cudaMemcpyHostToDevice) != cudaSuccess)
     return bail(fail(VX_ERR_CUDA, "upload failed"));
   h->fixed.assign((size_t)h->N, 0);
   h->fext.assign((size_t)h->N * 3, 0.0);
