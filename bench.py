@@ -222,8 +222,7 @@ def run_ours(args):
         nid = vd.bootstrap_nccl_id(dist, rank)
 
     sc = scene_for(args.config, args.precision)
-    if args.engine == "auto":
-        args.engine = "fused" if sc.cells.shape[0] >= 32 else "two_pass"
+    # "auto": the library's choice (VX_ENGINE_AUTO, resolved at the first step)
     if args.batch > 1:   # K copies of the scene packed along x, one launch per step (f2)
         from paper_1212_2845_b200.batch import pack
         lat = pack([sc] * args.batch, precision=args.precision, engine=args.engine,

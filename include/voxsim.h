@@ -222,8 +222,15 @@ int32_t vx_launches_per_step(const vx_lattice* h);
  * same arithmetic per bond and per voxel, same summation order.  Any nz
  * (taller than 256: z chunks of 256 voxels, each recomputing the -z bond of
  * its lowest layer).  In kernel timing (vx_kernel_times) the fused kernel is
- * reported in slot [1]. */
-typedef enum { VX_ENGINE_TWO_PASS = 0, VX_ENGINE_FUSED = 1 } vx_engine;
+ * reported in slot [1].
+ * VX_ENGINE_AUTO (the default): resolved once, at the first vx_step, to the
+ * faster of the two for this lattice -- fused when nz >= 64 or the lattice is
+ * split into slabs (then fused iff nz >= 32, the same choice on every rank);
+ * otherwise both are timed on the current state (as CUDA graphs, without
+ * advancing it) and the faster kept.  vx_get_engine returns VX_ENGINE_AUTO
+ * until it is resolved, then the engine in use.  Errors: INVALID_ARG for any
+ * other value. */
+typedef enum { VX_ENGINE_TWO_PASS = 0, VX_ENGINE_FUSED = 1, VX_ENGINE_AUTO = 2 } vx_engine;
 
 /* Batched independent scenes (the design-automation use of
  * "many, many physical evaluations"): the caller packs K scenes along x,

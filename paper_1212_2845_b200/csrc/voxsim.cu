@@ -166,7 +166,9 @@ struct vx_lattice {
   ncclComm_t comm = nullptr;
   long long steps_done = 0;
 
-  int engine = VX_ENGINE_TWO_PASS;
+  int engine = VX_ENGINE_FUSED;           // engine in use (provisional while AUTO is unresolved)
+  int engine_req = VX_ENGINE_AUTO;        // requested (vx_set_engine); AUTO resolves at the first step
+  bool engine_resolved = false;
   bool fused_smem_set[2] = {false, false};
   bool tma_ok = false;                    // TMA-staged fused variant (VX_FUSED_TMA=1; measured slower)
   int fused_ty = 8;                       // rows per fused block (VX_FUSED_TY overrides)
@@ -177,7 +179,6 @@ struct vx_lattice {
   int batch_stride = 0;                   // planes per batched scene (vx_set_batch)
 
   bool fused() const { return engine == VX_ENGINE_FUSED; }
-  bool fused_supported() const { return true; }   // any nz (z chunks of 256)
   void flip() {
     for (auto& s : slabs) s.par ^= 1;
   }
@@ -998,7 +999,91 @@ vx_status read_chunk_times(vx_lattice* h, size_t base, long long g) {
   return VX_OK;
 }
 
+vx_status sync_state_copies(vx_lattice* h);
+
+// VX_ENGINE_AUTO: pick the faster engine for this lattice once, at the first
+// step.  Lattices with full warps in z (nz >= 64) and slab-split lattices
+// (every rank must pick the same engine, so no timing) take the fused engine
+// when nz >= 32 (the design point: C5 1.24 vs 2.33 ms); otherwise both engines
+// are timed as CUDA graphs of the same 8 steps' kernels -- the fused pass after
+// its geometry tuning, the two-pass kernels on the spare state copy (K4 updates
+// in place) -- and the faster one is kept.  Small lattices go either way: one
+// C2 cube is faster fused (8.3 vs 11.4 us / step), 64 packed cubes or 4096
+// packed cantilevers (nz = 20, 1) are faster two-pass (34 vs 39, 9 vs 44 us).
+// Both engines produce the same S_{n+1}, so the choice only changes time.
+template <class R> vx_status resolve_engine(vx_lattice* h) {
+  if (h->engine_req != VX_ENGINE_AUTO || h->engine_resolved) return VX_OK;
+  h->engine_resolved = true;
+  h->clear_graphs();
+  if (h->emulated || h->nccl() || h->nz >= 64) {
+    h->engine = h->nz >= 32 ? VX_ENGINE_FUSED : VX_ENGINE_TWO_PASS;
+    return prepare(h);   // bond records of the two-pass engine
+  }
+  const bool col = h->collide();
+  Clock saved;
+  VX_CUDA(cudaMemcpy(&saved, h->clk.p, sizeof saved, cudaMemcpyDeviceToHost));
+  struct Ev {
+    cudaEvent_t e = nullptr;
+    ~Ev() { if (e) cudaEventDestroy(e); }
+  } ev0, ev1;
+  VX_CUDA(cudaEventCreate(&ev0.e));
+  VX_CUDA(cudaEventCreate(&ev1.e));
+  // 8 steps' kernels as one graph, launched once warm and 4 times timed
+  auto time_graph = [&](auto&& body, float* ms) -> vx_status {
+    cudaGraph_t g;
+    VX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    vx_status st = VX_OK;
+    for (int r = 0; r < 8 && st == VX_OK; ++r) st = body();
+    const cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
+    if (st != VX_OK) return st;
+    if (ce != cudaSuccess) return fail(VX_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    cudaGraphExec_t ex;
+    const cudaError_t ie = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) return fail(VX_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+    cudaGraphLaunch(ex, h->stream);
+    cudaEventRecord(ev0.e, h->stream);
+    for (int r = 0; r < 4; ++r) cudaGraphLaunch(ex, h->stream);
+    cudaEventRecord(ev1.e, h->stream);
+    const cudaError_t se = cudaEventSynchronize(ev1.e);
+    cudaGraphExecDestroy(ex);
+    if (se != cudaSuccess) return fail(VX_ERR_CUDA, std::string("engine timing: ") + cudaGetErrorString(se));
+    VX_CUDA(cudaEventElapsedTime(ms, ev0.e, ev1.e));
+    return VX_OK;
+  };
+  float t_fused = 0, t_two = 0;
+  h->engine = VX_ENGINE_FUSED;
+  VX_TRY(tune_fused<R>(h));
+  VX_TRY(time_graph([&]() -> vx_status {
+    for (const Slab& s : h->slabs) VX_TRY(launch_fused<R>(h, s, col, s.x0, s.x1));
+    return VX_OK;
+  }, &t_fused));
+  h->engine = VX_ENGINE_TWO_PASS;
+  VX_TRY(prepare(h));   // bond records
+  VX_TRY(sync_state_copies(h));
+  h->flip();
+  const vx_status st2 = time_graph([&]() -> vx_status {
+    for (const Slab& s : h->slabs) launch_bonds<R>(h, s, make_dev<R>(h, s), s.xl0, s.x1);
+    for (const Slab& s : h->slabs) launch_integrate<R>(h, s, make_dev<R>(h, s), col);
+    return VX_OK;
+  }, &t_two);
+  h->flip();
+  VX_TRY(st2);
+  VX_TRY(sync_state_copies(h));   // the spare copy back to S_n
+  VX_CUDA(cudaMemcpy(h->clk.p, &saved, sizeof saved, cudaMemcpyHostToDevice));
+  h->ss_dirty = true;
+  h->engine = t_two < t_fused ? VX_ENGINE_TWO_PASS : VX_ENGINE_FUSED;
+  if (h->fused())
+    for (Slab& s : h->slabs) { s.recA.release(); s.recB.release(); s.recC.release(); }
+  if (std::getenv("VX_FUSED_TUNE_LOG"))
+    std::fprintf(stderr, "voxsim: engine auto: fused %.2f us, two-pass %.2f us per step -> %s\n",
+                 1e3 * t_fused / 32, 1e3 * t_two / 32, h->fused() ? "fused" : "two_pass");
+  h->clear_graphs();
+  return VX_OK;
+}
+
 template <class R> vx_status run_steps(vx_lattice* h, long long n) {
+  VX_TRY(resolve_engine<R>(h));
   VX_TRY(tune_fused<R>(h));
   if (h->collide() && h->ss_dirty) VX_TRY(pack_surface<R>(h));
   // CUDA graphs of G steps; the remainder is captured as its own graph.  The
@@ -1715,14 +1800,17 @@ int32_t vx_num_scenes(const vx_lattice* h) {
 
 vx_status vx_set_engine(vx_lattice* h, int32_t engine) {
   if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
-  if (engine != VX_ENGINE_TWO_PASS && engine != VX_ENGINE_FUSED)
+  if (engine != VX_ENGINE_TWO_PASS && engine != VX_ENGINE_FUSED && engine != VX_ENGINE_AUTO)
     return fail(VX_ERR_INVALID_ARG, "unknown engine");
-  if (engine == VX_ENGINE_FUSED && !h->fused_supported())
-    return fail(VX_ERR_INVALID_ARG, "the fused engine needs nz <= 256");
-  h->engine = engine;
+  h->engine_req = engine;
+  h->engine_resolved = false;
+  if (engine != VX_ENGINE_AUTO) h->engine = engine;
   h->clear_graphs();
   return VX_OK;
 }
-int32_t vx_get_engine(const vx_lattice* h) { return h ? h->engine : -1; }
+int32_t vx_get_engine(const vx_lattice* h) {
+  if (!h) return -1;
+  return h->engine_req == VX_ENGINE_AUTO && !h->engine_resolved ? VX_ENGINE_AUTO : h->engine;
+}
 
 }  // extern "C"

@@ -800,23 +800,33 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
   R vmax = R(0);
   auto idx = [&](int i, int j) { return (uint32_t)i * sx + (uint32_t)j * nz + (uint32_t)k; };
 
-  // -x slots of plane i0: the +x bonds of plane i0 - 1 (halo, recomputed)
-  if (act)
-    for (int j = j0; j < j1; ++j) {
-      Rec6<R> r{};
-      if (i0 > 0) {
-        const uint32_t ia = idx(i0 - 1, j);
-        const VS<R> va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, ia);
-        if (meta_of(va.p.w) & nb_bit(1)) {
-          const VS<R> vb = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, ia + sx);
-          const AFrame<R> f = a_frame(d, va);
+  // -x slots of plane i0: the +x bonds of plane i0 - 1 (halo, recomputed); the
+  // next row's two voxels are loaded before this row's bond is evaluated
+  if (act) {
+    if (i0 > 0) {
+      VS<R> pa = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i0 - 1, j0));
+      VS<R> pb = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i0, j0));
+      for (int j = j0; j < j1; ++j) {
+        VS<R> na = pa, nb = pb;
+        if (j + 1 < j1) {
+          na = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i0 - 1, j + 1));
+          nb = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i0, j + 1));
+        }
+        Rec6<R> r{};
+        if (meta_of(pa.p.w) & nb_bit(1)) {
+          const AFrame<R> f = a_frame(d, pa);
           V3<R> Fa, Ma, Mb;
-          bond_eval<0>(d, f.Ra, va.q, f.ua, f.Va, f.wa, f.mat, vb, dT, Fa, Ma, Mb);
+          bond_eval<0>(d, f.Ra, pa.q, f.ua, f.Va, f.wa, f.mat, pb, dT, Fa, Ma, Mb);
           r = rec6(Fa, Mb);
         }
+        xrec[(size_t)(j - j0) * nzb + tk] = r;
+        pa = na;
+        pb = nb;
       }
-      xrec[(size_t)(j - j0) * nzb + tk] = r;
+    } else {
+      for (int j = j0; j < j1; ++j) xrec[(size_t)(j - j0) * nzb + tk] = Rec6<R>{};
     }
+  }
 
   for (int i = i0; i < i1; ++i) {
     VS<R> va, vb;    // ping-pong: this row's voxel and the next row's

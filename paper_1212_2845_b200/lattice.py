@@ -237,10 +237,11 @@ class Lattice:
     def num_scenes(self):
         return int(N.load().vx_num_scenes(self._h))
 
-    ENGINES = {"two_pass": 0, "fused": 1}
+    ENGINES = {"two_pass": 0, "fused": 1, "auto": 2}
 
     def set_engine(self, engine):
-        """'two_pass' (K3 + K4) or 'fused' (one kernel per step)."""
+        """'two_pass' (K3 + K4), 'fused' (one kernel per step) or 'auto' (the
+        default: the faster one for this lattice, chosen at the first step)."""
         _check(N.load().vx_set_engine(self._h, self.ENGINES.get(engine, engine)))
 
     @property
