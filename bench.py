@@ -225,8 +225,9 @@ def run_ours(args):
     # "auto": the library's choice (VX_ENGINE_AUTO, resolved at the first step)
     if args.batch > 1:   # K copies of the scene packed along x, one launch per step (f2)
         from paper_1212_2845_b200.batch import pack
-        lat = pack([sc] * args.batch, precision=args.precision, engine=args.engine,
-                   device=local).lattice
+        bt = pack([sc] * args.batch, precision=args.precision, engine=args.engine,
+                  device=local, z_stack=args.z_stack if args.z_stack == "auto" else int(args.z_stack))
+        lat = bt.lattice
     else:
         lat = from_scene(sc, precision=args.precision, device=local, rank=rank, nranks=world,
                          nccl_id=nid, init_state=sc.v0 is not None, engine=args.engine)
@@ -363,6 +364,8 @@ def run_ours(args):
                                    f"{sc.name} ({sc.cells.shape[2]}x{sc.cells.shape[1]}x"
                                    f"{sc.cells.shape[0]}, {N} voxels, {lat.num_bonds} bonds)",
                        "engine": lat.engine,
+                       **({"packing": f"{-(-args.batch // bt.z_stack)} x-blocks x {bt.z_stack} z-blocks"}
+                          if args.batch > 1 else {}),
                        "timing": "per-kernel CUDA events in the timed region" if live else
                                  "CUDA graphs; kernel breakdown from a separate instrumented pass",
                        "parallelism": f"x-slab{world}",
@@ -393,6 +396,8 @@ def main():
                     help="per-kernel events inside the timed region (live) or CUDA graphs")
     ap.add_argument("--batch", type=int, default=1,
                     help="pack K copies of the config into one lattice (SURVEY 8f f2)")
+    ap.add_argument("--z-stack", default="1",
+                    help="with --batch: scenes per z column ('auto' or an integer; 1 = along x only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0,

@@ -224,8 +224,9 @@ int32_t vx_launches_per_step(const vx_lattice* h);
  * its lowest layer).  In kernel timing (vx_kernel_times) the fused kernel is
  * reported in slot [1].
  * VX_ENGINE_AUTO (the default): resolved once, at the first vx_step, to the
- * faster of the two for this lattice -- fused when nz >= 64 or the lattice is
- * split into slabs (then fused iff nz >= 32, the same choice on every rank);
+ * faster of the two for this lattice -- fused when nz >= 64 and the lattice
+ * has >= 2^22 cells, or when it is split into slabs (then fused iff nz >= 32,
+ * the same choice on every rank);
  * otherwise both are timed on the current state (as CUDA graphs, without
  * advancing it) and the faster kept.  vx_get_engine returns VX_ENGINE_AUTO
  * until it is resolved, then the engine in use.  Errors: INVALID_ARG for any
@@ -241,6 +242,16 @@ typedef enum { VX_ENGINE_TWO_PASS = 0, VX_ENGINE_FUSED = 1, VX_ENGINE_AUTO = 2 }
  * stride 0 = one scene.  Errors: INVALID_ARG if a separator plane is not
  * empty.  All scenes share the environment, the time step and the clock. */
 vx_status vx_set_batch(vx_lattice* h, int32_t stride);
+/* Scenes stacked along z as well: every `stride` layers one scene, layer
+ * stride-1 of each block empty (no bonds cross it).  The fused engine runs one
+ * thread per z, so shallow scenes (nz < 32) stacked up to ~256 layers keep its
+ * warps full.  The floor of each stacked scene lies under its own
+ * lowest layer: its penetration is measured from the layer index within the
+ * block (k mod stride), so each scene sees what it would alone; self collision
+ * ignores pairs of different z blocks.  stride 0 = no z stacking.  Errors:
+ * INVALID_ARG if a separator layer is not empty.  vx_num_scenes counts x
+ * blocks times z blocks. */
+vx_status vx_set_batch_z(vx_lattice* h, int32_t stride);
 int32_t vx_num_scenes(const vx_lattice* h);
 vx_status vx_set_engine(vx_lattice* h, int32_t engine);
 int32_t vx_get_engine(const vx_lattice* h);

@@ -5,8 +5,13 @@ lattice runs the same kernels; ``vx_set_batch`` keeps self collision inside
 each scene.
 
 Every scene must share the grid shape, lattice dimension, origin and
-environment (one clock and one stable time step for the batch).  Scene s sits
-at x offset s * stride * l; the physics is invariant under that translation.
+environment (one clock and one stable time step for the batch).  Scenes sit on
+a grid of x blocks (``stride`` planes) and, for shallow scenes, z blocks
+(``stride_z`` layers, ``vx_set_batch_z``): the fused engine runs one thread per
+z, so stacking shallow scenes (nz < 32) up to ~256 layers keeps its warps full.
+The physics is invariant under the x translation; along z each scene's floor is
+placed under its own lowest layer by the library, so the z translation is
+invariant too.
 """
 from __future__ import annotations
 
@@ -23,10 +28,13 @@ class Batch:
     stride: int                 # planes per scene (nx + 1)
     counts: list                # voxels per scene
     ext_of: list                # per scene: packed external ids of its voxels (scene order)
-    offset: float               # x offset between consecutive scenes (m)
+    offset: float               # x offset between consecutive x blocks (m)
 
     rest: list = None           # per scene: packed rest sites of its voxels
     own: list = None            # per scene: its own rest sites (origin + l (ijk + 1/2))
+    stride_z: int = 0           # layers per z block (nz + 1), 0: no z stacking
+    z_stack: int = 1            # scenes per z column (scene s: x block s // z_stack,
+                                # z block s % z_stack)
 
     def state_of(self, s, st: State | None = None) -> State:
         """Scene s's state; positions as displacements from its packed rest sites
@@ -43,8 +51,22 @@ class Batch:
         return st.pos[self.ext_of[s]] - self.rest[s]
 
 
-def pack(scenes, precision=32, engine=None, device=0) -> Batch:
-    """Build one lattice holding every scene (see module docstring)."""
+def z_stack_for(K, nz, max_layers=256):
+    """Scenes per z column: 1 for nz >= 32; else as many as fit ``max_layers``
+    layers, balanced so the x blocks are evenly filled."""
+    if nz >= 32 or K <= 1:
+        return 1
+    kz = max(1, min(K, max_layers // (nz + 1)))
+    kx = -(-K // kz)
+    return -(-K // kx)
+
+
+def pack(scenes, precision=32, engine=None, device=0, z_stack=1) -> Batch:
+    """Build one lattice holding every scene (see module docstring).
+    ``z_stack``: scenes per z column (1: x only, the default; "auto":
+    ``z_stack_for``).  Measured (fp32, one B200): stacking helps
+    the fused engine (32 walkers 99 -> 78 us / step) but the two-pass engine,
+    faster for most mid-size batches, gains nothing from it."""
     s0 = scenes[0]
     nz, ny, nx = s0.cells.shape
     for sc in scenes:
@@ -54,6 +76,10 @@ def pack(scenes, precision=32, engine=None, device=0) -> Batch:
             raise ValueError("batched scenes must share environment and origin")
     stride = nx + 1
     K = len(scenes)
+    kz = z_stack_for(K, nz) if z_stack == "auto" else max(1, min(int(z_stack), K))
+    kx = -(-K // kz)
+    stride_z = nz + 1 if kz > 1 else 0
+    blk = [(s // kz, s % kz) for s in range(K)]             # (x block, z block) of scene s
     # material palette: union in first-seen order
     palette, remap = [], []
     for sc in scenes:
@@ -63,9 +89,10 @@ def pack(scenes, precision=32, engine=None, device=0) -> Batch:
                 palette.append(mat)
             m.append(palette.index(mat) + 1)
         remap.append(np.array([0] + m, np.uint8))
-    cells = np.zeros((nz, ny, K * stride - 1), np.uint8)
+    cells = np.zeros((kz * (nz + 1) - 1, ny, kx * stride - 1), np.uint8)
     for s, sc in enumerate(scenes):
-        cells[:, :, s * stride:s * stride + nx] = remap[s][sc.cells]
+        bx, bz = blk[s]
+        cells[bz * (nz + 1):bz * (nz + 1) + nz, :, bx * stride:bx * stride + nx] = remap[s][sc.cells]
     # packed external ids (x-fastest over the packed grid) of every scene voxel
     pid = -np.ones(cells.shape, np.int64)
     filled = cells > 0
@@ -73,7 +100,8 @@ def pack(scenes, precision=32, engine=None, device=0) -> Batch:
     ext_of = []
     for s, sc in enumerate(scenes):
         kk, jj, ii = np.nonzero(sc.cells)
-        ext_of.append(pid[kk, jj, ii + s * stride])
+        bx, bz = blk[s]
+        ext_of.append(pid[kk + bz * (nz + 1), jj, ii + bx * stride])
     N = int(filled.sum())
     l = s0.lattice_dim
     lat = Lattice.create_lattice(cells, l, s0.origin, precision, device)
@@ -82,6 +110,8 @@ def pack(scenes, precision=32, engine=None, device=0) -> Batch:
     if engine is not None:
         lat.set_engine(engine)
     lat.set_batch(stride)
+    if stride_z:
+        lat.set_batch_z(stride_z)
     fixed = np.zeros(N, np.uint8)
     fext = np.zeros((N, 3))
     pos = np.zeros((N, 3)); quat = np.zeros((N, 4)); lin = np.zeros((N, 3))
@@ -100,7 +130,8 @@ def pack(scenes, precision=32, engine=None, device=0) -> Batch:
         p, q, P, phi, la = sc.initial_state()
         ijk = sc.voxel_coords().astype(np.float64)
         own = org + l * (ijk + 0.5)                         # the scene's own rest sites
-        ijk[:, 0] += s * stride
+        ijk[:, 0] += blk[s][0] * stride
+        ijk[:, 2] += blk[s][1] * (nz + 1)
         packed = org + l * (ijk + 0.5)                      # its rest sites in the batch
         rest.append(packed)
         owns.append(own)
@@ -109,4 +140,5 @@ def pack(scenes, precision=32, engine=None, device=0) -> Batch:
     if any_bc:
         lat.set_boundary(fixed, fext)
     lat.set_state(pos, quat, lin, ang, latch)
-    return Batch(lat, stride, [len(e) for e in ext_of], ext_of, stride * l, rest, owns)
+    return Batch(lat, stride, [len(e) for e in ext_of], ext_of, stride * l, rest, owns,
+                 stride_z, kz)

@@ -177,6 +177,7 @@ struct vx_lattice {
   int fused_sx = 0;                       // fixed planes per segment (VX_FUSED_SX), 0: derived
   std::map<long long, std::pair<int, int>> geo_tuned;   // (TY, SX) chosen per launch range
   int batch_stride = 0;                   // planes per batched scene (vx_set_batch)
+  int batch_stride_z = 0;                 // layers per z-stacked scene (vx_set_batch_z)
 
   bool fused() const { return engine == VX_ENGINE_FUSED; }
   void flip() {
@@ -337,6 +338,7 @@ template <class R> Dev<R> make_dev(const vx_lattice* h, const Slab& s) {
   d.dt = (R)h->dt;
   d.l_d = h->l;
   d.zbase_d = h->origin[2] - h->env.floor_z;
+  d.bz = (uint32_t)h->batch_stride_z;
   d.floor_on = h->env_set ? h->env.floor_on : 0;
   d.ground = (h->env_set && h->env.zeta_ground > 0) ? 1 : 0;
   return d;
@@ -886,7 +888,7 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
     BroadArgs b{gb, S, h->rows_begin(), h->rows_end(), h->cellh.as<int4>(),
                 h->bcount.as<int>(), h->bstart.as<int>(), h->bitems.as<int>(),
                 h->rowptr.as<int>(), h->col.as<int>(), h->cap, h->H, h->clk.as<Clock>(),
-                h->batch_stride};
+                h->batch_stride, h->batch_stride_z};
     const double hc = h->cutoff * 1.001;
     {   // cooperative: all CTAs resident (grid-wide barriers between the phases)
       Dev<R> d0 = make_dev<R>(h, h->slabs[0]);
@@ -1002,9 +1004,10 @@ vx_status read_chunk_times(vx_lattice* h, size_t base, long long g) {
 vx_status sync_state_copies(vx_lattice* h);
 
 // VX_ENGINE_AUTO: pick the faster engine for this lattice once, at the first
-// step.  Lattices with full warps in z (nz >= 64) and slab-split lattices
-// (every rank must pick the same engine, so no timing) take the fused engine
-// when nz >= 32 (the design point: C5 1.24 vs 2.33 ms); otherwise both engines
+// step.  Large lattices with full warps in z (nz >= 64, >= 4M cells) and
+// slab-split lattices (every rank must pick the same engine, so no timing)
+// take the fused engine when nz >= 32 (the design point: C5 1.24 vs 2.33 ms);
+// otherwise both engines
 // are timed as CUDA graphs of the same 8 steps' kernels -- the fused pass after
 // its geometry tuning, the two-pass kernels on the spare state copy (K4 updates
 // in place) -- and the faster one is kept.  Small lattices go either way: one
@@ -1015,7 +1018,7 @@ template <class R> vx_status resolve_engine(vx_lattice* h) {
   if (h->engine_req != VX_ENGINE_AUTO || h->engine_resolved) return VX_OK;
   h->engine_resolved = true;
   h->clear_graphs();
-  if (h->emulated || h->nccl() || h->nz >= 64) {
+  if (h->emulated || h->nccl() || (h->nz >= 64 && h->nbox >= (1LL << 22))) {
     h->engine = h->nz >= 32 ? VX_ENGINE_FUSED : VX_ENGINE_TWO_PASS;
     return prepare(h);   // bond records of the two-pass engine
   }
@@ -1793,9 +1796,27 @@ vx_status vx_set_batch(vx_lattice* h, int32_t stride) {
   VX_TRY(set_device(h));
   return set_force_rebuild(h);
 }
+vx_status vx_set_batch_z(vx_lattice* h, int32_t stride) {
+  if (!h || stride < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
+  if (stride > 0) {
+    if (stride < 2) return fail(VX_ERR_INVALID_ARG, "a z-stacked scene needs >= 1 layer + a separator");
+    // every stride-th layer (stride-1, 2 stride-1, ...) must be empty
+    const size_t layer = (size_t)h->nx * h->ny;
+    for (int z = stride - 1; z < h->nz; z += stride)
+      for (size_t c = 0; c < layer; ++c)
+        if (h->cells[c + layer * (size_t)z])
+          return fail(VX_ERR_INVALID_ARG, "separator layer z=" + std::to_string(z) + " is not empty");
+  }
+  h->batch_stride_z = stride;
+  h->clear_graphs();
+  VX_TRY(set_device(h));
+  return set_force_rebuild(h);
+}
 int32_t vx_num_scenes(const vx_lattice* h) {
   if (!h) return -1;
-  return h->batch_stride ? (h->nx + h->batch_stride - 1) / h->batch_stride : 1;
+  const int kx = h->batch_stride ? (h->nx + h->batch_stride - 1) / h->batch_stride : 1;
+  const int kz = h->batch_stride_z ? (h->nz + h->batch_stride_z - 1) / h->batch_stride_z : 1;
+  return kx * kz;
 }
 
 vx_status vx_set_engine(vx_lattice* h, int32_t engine) {

@@ -60,6 +60,8 @@ template <class R> struct Dev {
                       // in fp64 so the fp32 rounding of l never strains the lattice
   double zbase_d;     // origin_z - floor_z
   int floor_on, ground;
+  uint32_t bz;        // layers per z-stacked batched scene (0: none): each scene's floor
+                      // sits under its own lowest layer
 };
 
 // ------------------------------------------------------------------ clock
@@ -533,9 +535,16 @@ __device__ __forceinline__ float integrate_store_f32(const Dev<float>& d, uint32
   return 0.f;
 }
 
+// Layer of global layer k within its z-stacked batched scene (vx_set_batch_z):
+// the floor lies under each scene's own lowest layer.
+template <class R> __device__ __forceinline__ uint32_t floor_layer(const Dev<R>& d, uint32_t k) {
+  return d.bz ? k % d.bz : k;
+}
+
 // After the slot sums (Eq. 25-26): external force, gravity, ground
 // damping (R12), contacts, floor + friction (R14, R15),
 // integration (Eq. 27-30); writes the new state of `id` to the out arrays.
+// kz: the voxel's layer within its scene (floor_layer).
 template <class R, bool COLLIDE>
 __device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, uint32_t kz, const VS<R>& s,
                                           uint32_t meta,
@@ -676,7 +685,7 @@ __global__ void __launch_bounds__(256) k_integrate(Dev<R> d, uint32_t beg, uint3
         }
       }
       s.q = d.quat[id];
-      vmax = finish_voxel<R, COLLIDE>(d, id, id % d.nz, s, meta, F, M, d.pos, d.quat, d.mom, d.ang,
+      vmax = finish_voxel<R, COLLIDE>(d, id, floor_layer(d, id % d.nz), s, meta, F, M, d.pos, d.quat, d.mom, d.ang,
                                       ext_of_local);
     }
   }
@@ -788,6 +797,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
   }
   const int k = kz0 + tk;
   const bool act = k < (int)d.nz;
+  const uint32_t kf = floor_layer(d, (uint32_t)k);   // once per thread: k is fixed
   const int tile = bid % a.ntiles_y;
   const int seg = bid / a.ntiles_y;
   const int j0 = tile * a.ty;
@@ -911,7 +921,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
       if (FULL || (meta & (M_FILLED | M_FIXED)) == M_FILLED) {
         if (meta & nb_bit(4)) slot_minus(F, M, (!ZC || tk > 0) ? zr[tk - 1] : zlo);
         if (meta & nb_bit(5)) slot_plus(F, M, FZ, MZ);
-        const R v = finish_voxel<R, COLLIDE>(d, id, k, cur, meta, F, M, a.opos, a.oquat, a.omom,
+        const R v = finish_voxel<R, COLLIDE>(d, id, kf, cur, meta, F, M, a.opos, a.oquat, a.omom,
                                              a.oang, a.ext_of_local);
         vmax = fmax(vmax, v);
       } else if (meta & M_FILLED) {   // fixed: copied through unchanged
@@ -1020,6 +1030,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R
 
   const int k = threadIdx.x;
   const bool act = k < (int)d.nz;
+  const uint32_t kf = floor_layer(d, (uint32_t)k);   // once per thread: k is fixed
   int bid = blockIdx.x, p0 = a.p0, p1 = a.p1;
   if (bid >= a.nblk0) { bid -= a.nblk0; p0 = a.p0b; p1 = a.p1b; }
   const int tile = bid % a.ntiles_y;
@@ -1136,7 +1147,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R
             slot_minus(F, M, z);
           }
           if (meta & nb_bit(5)) slot_plus(F, M, FZ, MZ);
-          const R v = finish_voxel<R, COLLIDE>(d, id, k, cur, meta, F, M, a.opos, a.oquat, a.omom,
+          const R v = finish_voxel<R, COLLIDE>(d, id, kf, cur, meta, F, M, a.opos, a.oquat, a.omom,
                                                a.oang, a.ext_of_local);
           vmax = fmax(vmax, v);
         } else if (meta & M_FILLED) {   // fixed: copied through unchanged
@@ -1191,6 +1202,7 @@ struct BroadArgs {
   int H;                  // power of two
   Clock* clk;
   int batch_stride;       // planes per batched scene (0: one scene); no cross-scene pairs
+  int batch_stride_z;     // layers per z-stacked batched scene (0: none)
 };
 
 __device__ __forceinline__ int cell_hash(int x, int y, int z, int H) {
@@ -1258,6 +1270,7 @@ __device__ __forceinline__ int bp_row(const Dev<R>& d, const BroadArgs& b,
           box_ijk(d, b.gbox[u], ib, jb, kb);
           if (abs(ia - ib) + abs(ja - jb) + abs(ka - kb) <= 3) continue;
           if (b.batch_stride && ia / b.batch_stride != ib / b.batch_stride) continue;
+          if (b.batch_stride_z && ka / b.batch_stride_z != kb / b.batch_stride_z) continue;
           const R4 pb = ss[2 * u];
           const R rx = d.l * (R)(ia - ib) + (pa.x - pb.x);
           const R ry = d.l * (R)(ja - jb) + (pa.y - pb.y);

@@ -233,6 +233,10 @@ class Lattice:
         """Declare K scenes packed along x, `stride` planes each (incl. separator)."""
         _check(N.load().vx_set_batch(self._h, int(stride)))
 
+    def set_batch_z(self, stride):
+        """Declare scenes stacked along z as well, `stride` layers each (incl. separator)."""
+        _check(N.load().vx_set_batch_z(self._h, int(stride)))
+
     @property
     def num_scenes(self):
         return int(N.load().vx_num_scenes(self._h))

@@ -21,12 +21,16 @@ def _cube_variants(K, n=6):
     return out
 
 
+@pytest.mark.parametrize("z_stack", [1, 2, "auto"])
 @pytest.mark.parametrize("engine", ["fused", "two_pass"])
 @pytest.mark.parametrize("prec", [32, 64])
-def test_batch_equals_each_scene_alone(engine, prec):
+def test_batch_equals_each_scene_alone(engine, prec, z_stack):
+    # the cubes rest on the floor (C2c): with z stacking each scene's floor
+    # lies under its own lowest layer
     scenes = _cube_variants(5)
-    b = pack(scenes, precision=prec, engine=engine)
-    assert b.lattice.num_scenes == 5
+    b = pack(scenes, precision=prec, engine=engine, z_stack=z_stack)
+    kz = {1: 1, 2: 2, "auto": 5}[z_stack]
+    assert b.z_stack == kz and b.lattice.num_scenes == (5 if kz != 2 else 6)
     b.lattice.step(120)
     st = b.lattice.read_state()
     for s, sc in enumerate(scenes):
@@ -41,11 +45,14 @@ def test_batch_equals_each_scene_alone(engine, prec):
         assert np.array_equal(st.latch[b.ext_of[s]], ref.latch)
 
 
-def test_batch_self_collision_stays_inside_each_scene():
+@pytest.mark.parametrize("z_stack", [1, "auto"])
+def test_batch_self_collision_stays_inside_each_scene(z_stack):
     # two-body collisions in every scene; bodies of neighbouring scenes are one
-    # plane apart, within the horizon, but must never be paired
+    # plane (or layer) apart, within the horizon, but must never be paired
     scenes = [W.two_bodies(v=v) for v in (1.5, 2.0, 2.5)]
-    b = pack(scenes, precision=64)
+    b = pack(scenes, precision=64, z_stack=z_stack)
+    if z_stack == "auto":
+        assert b.z_stack == 3
     b.lattice.step(300)
     st = b.lattice.read_state()
     pairs = b.lattice.contact_pairs()
@@ -65,3 +72,20 @@ def test_batch_rejects_filled_separator():
     lat = from_scene(sc, precision=32)
     with pytest.raises(VoxError):
         lat.set_batch(2)
+
+
+def test_batch_rejects_filled_separator_layer():
+    sc = W.cube(n=4)
+    lat = from_scene(sc, precision=32)
+    with pytest.raises(VoxError):
+        lat.set_batch_z(2)
+    lat.set_batch_z(0)
+
+
+def test_batch_z_stack_layout():
+    from paper_1212_2845_b200.batch import z_stack_for
+    assert z_stack_for(4096, 1) == 128          # 255 layers of cantilevers
+    assert z_stack_for(64, 20) == 11            # 6 x blocks of 11 cubes (64 scenes)
+    assert z_stack_for(32, 16) == 11            # 3 x blocks of 11 walkers
+    assert z_stack_for(100, 40) == 1            # deep scenes: x only
+    assert z_stack_for(1, 5) == 1

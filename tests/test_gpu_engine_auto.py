@@ -34,8 +34,6 @@ def test_auto_equals_the_engine_it_picks(name, prec):
     a.step(37)
     chosen = a.engine
     assert chosen in ("fused", "two_pass")
-    if sc.cells.shape[0] >= 64:      # nz >= 64: fused without timing
-        assert chosen == "fused"
     b = from_scene(sc, precision=prec, engine=chosen)
     b.step(37)
     assert np.array_equal(_flat(a.read_state()), _flat(b.read_state())), (name, chosen)
@@ -45,10 +43,16 @@ def test_auto_equals_the_engine_it_picks(name, prec):
     assert np.array_equal(_flat(a.read_state()), _flat(b.read_state()))
 
 
+def test_auto_takes_fused_for_large_deep_lattices():
+    lat = from_scene(W.block(64, 256, 256), precision=32)   # 2^22 cells, nz = 256
+    lat.step(2)
+    assert lat.engine == "fused"
+
+
 def test_auto_picks_two_pass_for_packed_cantilevers():
     # 4096 packed cantilevers (nz = 1): the fused pass runs 1 of 32 lanes per
     # warp (44 us / step), the two-pass kernels full warps (9 us / step)
-    bt = pack([W.cantilever()] * 4096, precision=32)
+    bt = pack([W.cantilever()] * 4096, precision=32, z_stack=1)
     bt.lattice.step(3)
     assert bt.lattice.engine == "two_pass"
 
