@@ -291,8 +291,7 @@ def run_ours(args):
         try:
             tr = json.load(open(tp))
             t = tr.get(f"{args.config}:fp{args.precision}:{dom}")
-            traffic = t / (1e-3 * per_step_ms[dom]) / 1e9 if t else None   # ncu bytes -> GB/s
-            traffic = {"bytes_per_launch": t, "GBps_at_live_time": traffic} if t else None
+            traffic = float(t) if t else None   # ncu dram bytes read + written per launch
         except Exception:
             traffic = None
     names = {"bonds": "k_bonds (K3)", "integrate": "k_integrate (K4)",
@@ -300,6 +299,7 @@ def run_ours(args):
     roof = {"bound": "hbm", "kernel": names[dom],
             "achieved": gbps[dom], "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": gbps[dom] / peak, "traffic": traffic,
+            "traffic_bytes_per_voxel": traffic / vox_rank if traffic else None,
             "alg_bytes_per_voxel": alg[dom], "avg_launch_ms": avg[dom],
             "kernels": {k: {"ms_per_step": per_step_ms[k], "GBps": gbps[k]} for k in kinds},
             "step_GBps_alg": sum(alg[k] for k in kinds) * N / (ms_max / args.steps / 1e3) / 1e9}
@@ -308,7 +308,7 @@ def run_ours(args):
         alu = alu_roof(args.precision, per_step_ms[dom], vox_rank, clocks)
         if alu:
             hbm = {k: roof[k] for k in ("bound", "achieved", "peak", "peak_source", "unit", "frac",
-                                        "traffic", "alg_bytes_per_voxel")}
+                                        "traffic", "traffic_bytes_per_voxel", "alg_bytes_per_voxel")}
             roof.update({k: alu[k] for k in ("bound", "achieved", "peak", "unit", "frac")})
             roof["peak_source"] = alu["peak_note"]
             roof["alu"] = alu

@@ -32,6 +32,7 @@ def test_bench_line_ours():
     assert d["gpu_launches"] > 0
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
+    assert r["traffic"] is None or isinstance(r["traffic"], float)   # ncu bytes per launch
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
