@@ -9,10 +9,15 @@ Python side of the oracle: a ctypes wrapper around ``oracle.cpp`` (the stepper,
 written from the paper step by step) plus the plain-numpy direct stiffness
 method (``oracle.dsm``) and the cantilever elastica (``oracle.elastica``).
 
-Functions whose parity is not pinned by the paper or by mathematics:
-    the floor friction constants and the self-collision penalty law
-     -- "parity unpinned" beyond the closed-form
-    single-voxel checks in tests/test_oracle_pins.py.
+Pins (tests/test_oracle_pins.py; DESIGN.md §6 lists them per function): every
+oracle function is checked against something other than itself -- the paper's
+worked examples and tables (tests/golden/), closed forms, invariants, brute
+force.  The floor penalty constants (R14), the friction law's constants (R15)
+and the self-collision penalty law (the paper leaves
+them open) are readings: they are pinned to the closed forms of the reading
+(resting penetration m g / k_f, the Eq. 38 halting threshold, breakaway at
+mu_s F_n and deceleration mu_d g, one pair's penalty force and momentum
+balance, the brute-force pair definition), not to a number the paper prints.
 """
 from __future__ import annotations
 
