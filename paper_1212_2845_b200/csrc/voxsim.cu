@@ -146,7 +146,7 @@ struct vx_lattice {
   // self collision: global surface table (kernels K5 / k_contact)
   std::vector<unsigned> surf_g;           // global box id of every surface voxel, ascending
   std::vector<int> seg;                   // nranks + 1: surface segment of each rank's slab
-  DevBuf surf_d, ss, cellh, bcount, bstart, bitems, rowptr, col;
+  DevBuf surf_d, sijk, ss, cellh, bcount, bstart, bitems, rowptr, col;
   int H = 0;
   int bp_grid = 1;                        // CTAs of the cooperative broadphase
   bool ss_dirty = true;                   // the surface table must be re-packed from the state
@@ -526,6 +526,15 @@ vx_status setup_collision(vx_lattice* h) {
   const size_t r = rsize(h->prec);
   VX_TRY(h->surf_d.alloc((size_t)std::max(S, 1) * 4));
   if (S) VX_CUDA(cudaMemcpy(h->surf_d.p, h->surf_g.data(), (size_t)S * 4, cudaMemcpyHostToDevice));
+  {   // lattice coordinates of every surface entry (the contact kernel's table)
+    std::vector<int4> ijk((size_t)std::max(S, 1));
+    for (int s = 0; s < S; ++s) {
+      const unsigned g = h->surf_g[s];
+      ijk[s] = make_int4((int)(g / h->plane), (int)((g / h->nz) % h->ny), (int)(g % h->nz), 0);
+    }
+    VX_TRY(h->sijk.alloc(ijk.size() * sizeof(int4)));
+    VX_CUDA(cudaMemcpy(h->sijk.p, ijk.data(), ijk.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  }
   VX_TRY(h->ss.alloc((size_t)std::max(S, 1) * 2 * 4 * r));
   int H = 1024;
   while (H < 2 * S) H <<= 1;
@@ -902,7 +911,8 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
     for (size_t q = 0; q < h->slabs.size(); ++q) {
       const int s0 = h->slab_seg(q, 0), s1 = h->slab_seg(q, 1);
       if (s1 > s0)
-        k_contact<R><<<grid_of(s1 - s0), 256, 0, h->stream>>>(make_dev<R>(h, h->slabs[q]), gb, ss, s0, s1,
+        k_contact<R><<<grid_of((long long)(s1 - s0) * CONTACT_LANES), 256, 0, h->stream>>>(
+            make_dev<R>(h, h->slabs[q]), gb, h->sijk.as<int4>(), ss, s0, s1,
                                                                h->rowptr.as<int>(), h->col.as<int>(),
                                                                (R)h->env.zeta_col);
     }

@@ -1356,54 +1356,62 @@ __global__ void __launch_bounds__(1024, 1) k_broadphase(Dev<R> d, BroadArgs b, c
 // q = r_a + r_b - |D_a - D_b|; partners summed in ascending surface index
 // (= ascending box id).  Rows [r0, r1) are one slab's segment; the load goes
 // to that slab's cf at the voxel's local id.
+// Contact loads of surface row s (row a7): the pair law over its CSR partners.
+// CONTACT_LANES lanes share a row: lane c takes partners c, c + L, c + 2L, ...
+// of the ascending partner list, and the L partial sums are combined by a fixed
+// butterfly -- deterministic, the same on every engine and slab count (one
+// kernel), and equal to the oracle's ascending sum up to rounding.  The lattice
+// coordinates of surface entries come from a table (sijk), not divisions.
+constexpr int CONTACT_LANES = 8;
 template <class R>
-__device__ __forceinline__ void contact_row(const Dev<R>& d, const unsigned* gbox,
-                                            const typename VT<R>::R4* ss, int s, const int* rowptr,
-                                            const int* col, R zeta_col) {
-  using R4 = typename VT<R>::R4;
-  int ia, ja, ka;
-  box_ijk(d, gbox[s], ia, ja, ka);
-  const R4 pa = ss[2 * s];
-  const int mat_a = meta_of(pa.w) & M_MAT;
-  const MatC<R>& ma = d.mat[mat_a];
-  const R4 moa = ss[2 * s + 1];
-  const R dT = (R)d.clk->dT;
-  const R ra = d.half_l * (R(1) + ma.alpha * dT);
-  V3<R> F = mk(R(0), R(0), R(0));
-  for (int q = rowptr[s]; q < rowptr[s + 1]; ++q) {
-    const int u = col[q];
-    int ib, jb, kb;
-    box_ijk(d, gbox[u], ib, jb, kb);
-    const R4 pb = ss[2 * u];
-    const int mat_b = meta_of(pb.w) & M_MAT;
-    const MatC<R>& mb = d.mat[mat_b];
-    const R rb = d.half_l * (R(1) + mb.alpha * dT);
-    const V3<R> dd = mk(d.l * (R)(ia - ib) + (pa.x - pb.x), d.l * (R)(ja - jb) + (pa.y - pb.y),
-                        d.l * (R)(ka - kb) + (pa.z - pb.z));
-    const R dist = vx_sqrt(dot(dd, dd));
-    const R pen = ra + rb - dist;
-    if (!(pen > R(0))) continue;
-    V3<R> n;
-    if (dist > R(0)) n = (R(1) / dist) * dd;
-    else n = mk(R(0), R(0), s < u ? R(1) : R(-1));
-    const R4 mob = ss[2 * u + 1];
-    const V3<R> Va = ma.inv_m * mk(moa.x, moa.y, moa.z);
-    const V3<R> Vb = mb.inv_m * mk(mob.x, mob.y, mob.z);
-    const R vn = dot(Va - Vb, n);
-    const R kc = R(2) * ma.kc * mb.kc / (ma.kc + mb.kc);
-    const R cc = R(2) * zeta_col * vx_sqrt(fmin(ma.m, mb.m) * kc);
-    R f = kc * pen - cc * vn;
-    if (f < R(0)) f = R(0);
-    F = F + f * n;
-  }
-  d.cf[gbox[s] - (unsigned)d.xl0 * d.sx] = R4{F.x, F.y, F.z, R(0)};
-}
-template <class R>
-__global__ void __launch_bounds__(256) k_contact(Dev<R> d, const unsigned* gbox,
+__global__ void __launch_bounds__(256) k_contact(Dev<R> d, const unsigned* gbox, const int4* sijk,
                                                  const typename VT<R>::R4* ss, int r0, int r1,
                                                  const int* rowptr, const int* col, R zeta_col) {
-  const int s = r0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < r1) contact_row(d, gbox, ss, s, rowptr, col, zeta_col);
+  using R4 = typename VT<R>::R4;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = r0 + t / CONTACT_LANES, c = t % CONTACT_LANES;
+  const bool row = s < r1;
+  V3<R> F = mk(R(0), R(0), R(0));
+  if (row) {
+    const int4 a = sijk[s];
+    const R4 pa = ss[2 * s];
+    const MatC<R>& ma = d.mat[meta_of(pa.w) & M_MAT];
+    const R4 moa = ss[2 * s + 1];
+    const R dT = (R)d.clk->dT;
+    const R ra = d.half_l * (R(1) + ma.alpha * dT);
+    const int q1 = rowptr[s + 1];
+    for (int q = rowptr[s] + c; q < q1; q += CONTACT_LANES) {
+      const int u = col[q];
+      const int4 b = sijk[u];
+      const R4 pb = ss[2 * u];
+      const MatC<R>& mb = d.mat[meta_of(pb.w) & M_MAT];
+      const R rb = d.half_l * (R(1) + mb.alpha * dT);
+      const V3<R> dd = mk(d.l * (R)(a.x - b.x) + (pa.x - pb.x), d.l * (R)(a.y - b.y) + (pa.y - pb.y),
+                          d.l * (R)(a.z - b.z) + (pa.z - pb.z));
+      const R dist = vx_sqrt(dot(dd, dd));
+      const R pen = ra + rb - dist;
+      if (!(pen > R(0))) continue;
+      V3<R> n;
+      if (dist > R(0)) n = (R(1) / dist) * dd;
+      else n = mk(R(0), R(0), s < u ? R(1) : R(-1));
+      const R4 mob = ss[2 * u + 1];
+      const V3<R> Va = ma.inv_m * mk(moa.x, moa.y, moa.z);
+      const V3<R> Vb = mb.inv_m * mk(mob.x, mob.y, mob.z);
+      const R vn = dot(Va - Vb, n);
+      const R kc = R(2) * ma.kc * mb.kc / (ma.kc + mb.kc);
+      const R cc = R(2) * zeta_col * vx_sqrt(fmin(ma.m, mb.m) * kc);
+      R f = kc * pen - cc * vn;
+      if (f < R(0)) f = R(0);
+      F = F + f * n;
+    }
+  }
+#pragma unroll
+  for (int o = CONTACT_LANES / 2; o > 0; o >>= 1) {
+    F.x = F.x + __shfl_xor_sync(0xffffffffu, F.x, o);
+    F.y = F.y + __shfl_xor_sync(0xffffffffu, F.y, o);
+    F.z = F.z + __shfl_xor_sync(0xffffffffu, F.z, o);
+  }
+  if (row && c == 0) d.cf[gbox[s] - (unsigned)d.xl0 * d.sx] = R4{F.x, F.y, F.z, R(0)};
 }
 
 // ------------------------------------------------------------------ state I/O
