@@ -27,7 +27,7 @@ SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "ms": 1e-3, "us": 
 
 
 def short(name):
-    return name.split("(")[0].split("<")[0].replace("void ", "").strip()
+    return name.split("(")[0].split("<")[0].replace("void ", "").replace("vx::", "").strip()
 
 
 def launches(path):
