@@ -442,7 +442,7 @@ template <class R> vx_status upload_tables(vx_lattice* h) {
       double a1, a2, b1, b2, b3;
       pair_consts(md[i], md[j], l, &a1, &a2, &b1, &b2, &b3);
       PairC<R>& p = pc[(size_t)i * n + j];
-      p.a1 = (R)a1; p.a2 = (R)a2; p.b1 = (R)b1; p.b2 = (R)b2; p.b3 = (R)b3;
+      p.a1 = (R)a1; p.a2 = (R)a2; p.b1 = (R)b1; p.b2 = (R)b2; p.nb2 = -(R)b2; p.b3 = (R)b3;
       p.alpha_mean = (R)(0.5 * (md[i].cte + md[j].cte));
       const double mmin = std::min(md[i].m, md[j].m), Imin = std::min(md[i].I, md[j].I);
       const double ct = 2 * e.zeta_bond * std::sqrt(mmin * a1);   // Eq. 34, R10
@@ -452,7 +452,6 @@ template <class R> vx_status upload_tables(vx_lattice* h) {
       p.cr2 = (R)(0.5 * cr);
       p.inv_m_b = (R)(1.0 / md[j].m);
       p.inv_I_b = (R)(1.0 / md[j].I);
-      p.pad0 = (R)0;
       if (h->pair_present[(size_t)i * 256 + j]) {   // Eq. 40 fault bounds
         h->alpha_lo = std::min(h->alpha_lo, 0.5 * (md[i].cte + md[j].cte));
         h->alpha_hi = std::max(h->alpha_hi, 0.5 * (md[i].cte + md[j].cte));

@@ -67,13 +67,14 @@ template <class R> struct __align__(16) MatC {
   R pad0, pad1;
 };
 // Per ordered material-pair (a, b) constants (Eq. 1-12, 34-35, 40).
+// Laid out so (a1, a2) and (nb2, b2) are aligned pairs for the FP32x2 bond.
 template <class R> struct __align__(16) PairC {
-  R a1, a2, b1, b2, b3;
+  R a1, a2, nb2, b2;              // nb2 = -b2
+  R b1, b3;
   R alpha_mean;                   // (alpha_1 + alpha_2) / 2
   R ct2, ct4, cr2;                // c_t/2, c_t/4, c_r/2 with c_t = 2 zeta_b sqrt(m_min a1),
                                   // c_r = 2 zeta_b sqrt(I_min a2)
   R inv_m_b, inv_I_b;             // 1/m, 1/I of material b (damping velocities)
-  R pad0;
 };
 
 // ---------------------------------------------------------------- vec3

@@ -296,12 +296,21 @@ __device__ __forceinline__ void bond_eval(const Dev<float>& d, const RotP& Ra, c
   const float X2 = xsub(dv.x, xmul(xmul(l, c.alpha_mean), dT));
   const float Y2 = dv.y, Z2 = dv.z;
   const float b3x2 = 2.f * c.b3;
-  const V3<float> fa = mk(xmul(c.a1, X2), xfma(-c.b2, th.z, xmul(c.b1, Y2)),
-                          xfma(c.b2, th.y, xmul(c.b1, Z2)));
-  const V3<float> ma = mk(xmul(c.a2, th.x), xfma(-c.b3, th.y, xmul(-c.b2, Z2)),
-                          xfma(-c.b3, th.z, xmul(c.b2, Y2)));
-  const V3<float> mbl = mk(xmul(-c.a2, th.x), xfma(-b3x2, th.y, xmul(-c.b2, Z2)),
-                           xfma(-b3x2, th.z, xmul(c.b2, Y2)));
+  // the generic formulas, paired (same roundings, lane by lane):
+  //   (fa.x, ma.x) = (a1, a2) (X2, th.x);  mbl.x = -ma.x (exact)
+  //   (fa.y, fa.z) = (-b2, b2) (th.z, th.y) + b1 (Y2, Z2)
+  //   (ma.y, ma.z) = -b3 (th.y, th.z) + (-b2, b2) (Z2, Y2)
+  //   (mbl.y, mbl.z) = -2 b3 (th.y, th.z) + (-b2, b2) (Z2, Y2)
+  const f2_t nbb = f2pk(c.nb2, c.b2);
+  const f2_t xa = mul2(f2pk(c.a1, c.a2), f2pk(X2, th.x));
+  const f2_t fyz = fma2(nbb, f2pk(th.z, th.y), mul2(bc2(c.b1), f2pk(Y2, Z2)));
+  const f2_t pzy = mul2(nbb, f2pk(Z2, Y2));
+  const f2_t thyz = f2pk(th.y, th.z);
+  const f2_t myz = fma2(bc2(-c.b3), thyz, pzy);
+  const f2_t byz = fma2(bc2(-b3x2), thyz, pzy);
+  const V3<float> fa = mk(f2lo(xa), f2lo(fyz), f2hi(fyz));
+  const V3<float> ma = mk(f2hi(xa), f2lo(myz), f2hi(myz));
+  const V3<float> mbl = mk(-f2hi(xa), f2lo(byz), f2hi(byz));
   Fa = mul(Ra, to_world<AX>(fa));
   Ma = mul(Ra, to_world<AX>(ma));
   Mbw = mul(Ra, to_world<AX>(mbl));
