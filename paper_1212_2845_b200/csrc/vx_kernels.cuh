@@ -549,13 +549,18 @@ __device__ __forceinline__ float integrate_store_f32(const Dev<float>& d, uint32
 template <class R> __device__ __forceinline__ uint32_t floor_layer(const Dev<R>& d, uint32_t k) {
   return d.bz ? k % d.bz : k;
 }
+// Height of the rest site of layer k above the floor, D0_z - z_floor, formed in
+// fp64 (Dev::l_d) and rounded to R once; layer k within its scene (floor_layer).
+template <class R> __device__ __forceinline__ R floor_base(const Dev<R>& d, uint32_t k) {
+  return (R)(d.zbase_d + d.l_d * (double)floor_layer(d, k));
+}
 
 // After the slot sums (Eq. 25-26): external force, gravity, ground
 // damping (R12), contacts, floor + friction (R14, R15),
 // integration (Eq. 27-30); writes the new state of `id` to the out arrays.
-// kz: the voxel's layer within its scene (floor_layer).
+// zb: floor_base of the voxel's layer (the fused pass forms it once per thread).
 template <class R, bool COLLIDE>
-__device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, uint32_t kz, const VS<R>& s,
+__device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, R zb, const VS<R>& s,
                                           uint32_t meta,
                                           V3<R> F, V3<R> M, typename VT<R>::R4* __restrict__ opos,
                                           typename VT<R>::R4* __restrict__ oquat,
@@ -600,8 +605,7 @@ __device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, uint32_t
   if (d.floor_on) {                                   // P:260-274, R14, R15
     const R dT = (R)d.clk->dT;
     // penetration r_v - (D_z - z_floor), r_v = (l/2)(1 + alpha dT)
-    const R base = (R)(d.zbase_d + d.l_d * (double)kz);
-    const R pen = d.half_l * mc.alpha * dT - p.z - base;
+    const R pen = d.half_l * mc.alpha * dT - p.z - zb;
     if (pen > R(0)) {
       R Fn = mc.kf * pen - mc.cfl * V.z;
       if (Fn < R(0)) Fn = R(0);
@@ -694,7 +698,7 @@ __global__ void __launch_bounds__(256) k_integrate(Dev<R> d, uint32_t beg, uint3
         }
       }
       s.q = d.quat[id];
-      vmax = finish_voxel<R, COLLIDE>(d, id, floor_layer(d, id % d.nz), s, meta, F, M, d.pos, d.quat, d.mom, d.ang,
+      vmax = finish_voxel<R, COLLIDE>(d, id, floor_base(d, id % d.nz), s, meta, F, M, d.pos, d.quat, d.mom, d.ang,
                                       ext_of_local);
     }
   }
@@ -806,7 +810,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
   }
   const int k = kz0 + tk;
   const bool act = k < (int)d.nz;
-  const uint32_t kf = floor_layer(d, (uint32_t)k);   // once per thread: k is fixed
+  const R kf = floor_base(d, (uint32_t)k);   // once per thread: k is fixed
   const int tile = bid % a.ntiles_y;
   const int seg = bid / a.ntiles_y;
   const int j0 = tile * a.ty;
@@ -1039,7 +1043,7 @@ __global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R
 
   const int k = threadIdx.x;
   const bool act = k < (int)d.nz;
-  const uint32_t kf = floor_layer(d, (uint32_t)k);   // once per thread: k is fixed
+  const R kf = floor_base(d, (uint32_t)k);   // once per thread: k is fixed
   int bid = blockIdx.x, p0 = a.p0, p1 = a.p1;
   if (bid >= a.nblk0) { bid -= a.nblk0; p0 = a.p0b; p1 = a.p1b; }
   const int tile = bid % a.ntiles_y;
