@@ -188,7 +188,7 @@ def run_reference(args):
         desc = f"{sc.name} full lattice"
     from oracle import OracleSim as O
     o = O(sc.cells, sc.lattice_dim, sc.materials, sc.env, sc.origin)
-    threads = threads or os.cpu_count() or 1
+    threads = os.cpu_count() or 1
     o.set_threads(threads)
     if sc.fixed is not None or sc.fext is not None:
         o.set_boundary(sc.fixed, sc.fext)
@@ -206,7 +206,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config} (oracle sample: {desc})"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": f"{desc}, {args.steps} timed steps"},
+                         "sample": f"{desc}, {args.steps} timed steps", "cpu_model": cpu_model()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -896,7 +896,7 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
     BroadArgs b{gb, S, h->rows_begin(), h->rows_end(), h->cellh.as<int4>(),
                 h->bcount.as<int>(), h->bstart.as<int>(), h->bitems.as<int>(),
                 h->rowptr.as<int>(), h->col.as<int>(), h->cap, h->H, h->clk.as<Clock>(),
-                h->batch_stride, h->batch_stride_z};
+                h->batch_stride, h->batch_stride_z, h->sijk.as<int4>()};
     const double hc = h->cutoff * 1.001;
     {   // cooperative: all CTAs resident (grid-wide barriers between the phases)
       Dev<R> d0 = make_dev<R>(h, h->slabs[0]);

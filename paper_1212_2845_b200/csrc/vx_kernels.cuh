@@ -1216,6 +1216,7 @@ struct BroadArgs {
   Clock* clk;
   int batch_stride;       // planes per batched scene (0: one scene); no cross-scene pairs
   int batch_stride_z;     // layers per z-stacked batched scene (0: none)
+  const int4* sijk;       // S lattice coordinates (i, j, k) of the surface entries
 };
 
 __device__ __forceinline__ int cell_hash(int x, int y, int z, int H) {
@@ -1261,47 +1262,77 @@ __device__ __forceinline__ void box_ijk(const Dev<R>& d, unsigned g, int& i, int
 // Partners of surface voxel s (global surface indices u != s in the 27 cells
 // around it with |D_s - D_u| < cutoff and lattice Manhattan distance > 3):
 // counted (FILL = false) or written to col[base..) and sorted ascending.
+// BP_LANES lanes share a row: lane c queries the cells c, c + L, ... of the 27
+// around it (dz, dy, dx order).  The count pass sums the lanes' counts; the
+// fill pass writes each lane's partners at its exclusive prefix and lane 0
+// sorts the row ascending, so the row is the same set in the same order for
+// any lane split (deterministic).  All lanes of a warp call this together.
+constexpr int BP_LANES = 8;
 template <bool FILL, class R>
 __device__ __forceinline__ int bp_row(const Dev<R>& d, const BroadArgs& b,
-                                      const typename VT<R>::R4* ss, int s, R cutoff2, int base) {
+                                      const typename VT<R>::R4* ss, int s, bool act, int c, R cutoff2,
+                                      int base) {
   using R4 = typename VT<R>::R4;
-  const int4 cs = b.cellh[s];
-  int ia, ja, ka;
-  box_ijk(d, b.gbox[s], ia, ja, ka);
-  const R4 pa = ss[2 * s];
   int cnt = 0;
-  for (int dz = -1; dz <= 1; ++dz)
-    for (int dy = -1; dy <= 1; ++dy)
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int cx = cs.x + dx, cy = cs.y + dy, cz = cs.z + dz;
-        const int hh = cell_hash(cx, cy, cz, b.H);
-        for (int q = b.bstart[hh]; q < b.bstart[hh + 1]; ++q) {
-          const int u = b.bitems[q];
-          const int4 cu = b.cellh[u];
-          if (u == s || cu.x != cx || cu.y != cy || cu.z != cz) continue;
-          int ib, jb, kb;
-          box_ijk(d, b.gbox[u], ib, jb, kb);
-          if (abs(ia - ib) + abs(ja - jb) + abs(ka - kb) <= 3) continue;
-          if (b.batch_stride && ia / b.batch_stride != ib / b.batch_stride) continue;
-          if (b.batch_stride_z && ka / b.batch_stride_z != kb / b.batch_stride_z) continue;
-          const R4 pb = ss[2 * u];
-          const R rx = d.l * (R)(ia - ib) + (pa.x - pb.x);
-          const R ry = d.l * (R)(ja - jb) + (pa.y - pb.y);
-          const R rz = d.l * (R)(ka - kb) + (pa.z - pb.z);
-          if (rx * rx + ry * ry + rz * rz >= cutoff2) continue;
-          if (FILL && base + cnt < b.cap) b.col[base + cnt] = u;
-          ++cnt;
-        }
+  int4 cs = make_int4(0, 0, 0, 0), a = cs;
+  R4 pa{};
+  if (act) {
+    cs = b.cellh[s];
+    a = b.sijk[s];
+    pa = ss[2 * s];
+  }
+  // the lane's candidates, twice: count, then (FILL) write at the prefix
+  auto scan = [&](bool write, int at) {
+    int n = 0;
+    for (int ci = c; act && ci < 27; ci += BP_LANES) {
+      const int cx = cs.x + ci % 3 - 1, cy = cs.y + (ci / 3) % 3 - 1, cz = cs.z + ci / 9 - 1;
+      const int hh = cell_hash(cx, cy, cz, b.H);
+      for (int q = b.bstart[hh]; q < b.bstart[hh + 1]; ++q) {
+        const int u = b.bitems[q];
+        const int4 cu = b.cellh[u];
+        if (u == s || cu.x != cx || cu.y != cy || cu.z != cz) continue;
+        const int4 o = b.sijk[u];
+        if (abs(a.x - o.x) + abs(a.y - o.y) + abs(a.z - o.z) <= 3) continue;
+        if (b.batch_stride && a.x / b.batch_stride != o.x / b.batch_stride) continue;
+        if (b.batch_stride_z && a.z / b.batch_stride_z != o.z / b.batch_stride_z) continue;
+        const R4 pb = ss[2 * u];
+        const R rx = d.l * (R)(a.x - o.x) + (pa.x - pb.x);
+        const R ry = d.l * (R)(a.y - o.y) + (pa.y - pb.y);
+        const R rz = d.l * (R)(a.z - o.z) + (pa.z - pb.z);
+        if (rx * rx + ry * ry + rz * rz >= cutoff2) continue;
+        if (write && at + n < b.cap) b.col[at + n] = u;
+        ++n;
       }
-  if (FILL && base + cnt <= b.cap) {   // sort the row by partner index (deterministic)
-    for (int x = base + 1; x < base + cnt; ++x) {
+    }
+    return n;
+  };
+  const int lane = threadIdx.x & 31, g0 = lane & ~(BP_LANES - 1);
+  const unsigned gm = ((1u << BP_LANES) - 1u) << g0;   // this row's lanes
+  cnt = scan(false, 0);
+  if (!FILL) {
+#pragma unroll
+    for (int o = BP_LANES / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    return cnt;
+  }
+  // exclusive prefix of the lane counts within the row's lanes
+  int pre = cnt;
+#pragma unroll
+  for (int o = 1; o < BP_LANES; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, pre, o);
+    if ((lane & (BP_LANES - 1)) >= o) pre += v;
+  }
+  const int tot = __shfl_sync(0xffffffffu, pre, g0 + BP_LANES - 1);
+  scan(true, base + pre - cnt);
+  __syncwarp(gm);
+  if (act && c == 0 && base + tot <= b.cap) {   // sort the row by partner index (deterministic)
+    for (int x = base + 1; x < base + tot; ++x) {
       const int v = b.col[x];
       int y = x - 1;
       while (y >= base && b.col[y] > v) { b.col[y + 1] = b.col[y]; --y; }
       b.col[y + 1] = v;
     }
   }
-  return cnt;
+  return tot;
 }
 
 // Cooperative launch over the whole GPU (grid-wide barriers between phases),
@@ -1316,8 +1347,8 @@ __device__ __forceinline__ void broadphase_phases(const Dev<R>& d, const BroadAr
   for (int x = tid; x < b.H; x += nth) b.bcount[x] = 0;
   g.sync();
   for (int s = tid; s < b.S; s += nth) {
-    int i, j, k;
-    box_ijk(d, b.gbox[s], i, j, k);
+    const int4 ijk = b.sijk[s];
+    const int i = ijk.x, j = ijk.y, k = ijk.z;
     const R4 p = ss[2 * s];
     const R Dx = (R)(ox + d.l_d * ((double)i + 0.5)) + p.x;
     const R Dy = (R)(oy + d.l_d * ((double)j + 0.5)) + p.y;
@@ -1340,8 +1371,16 @@ __device__ __forceinline__ void broadphase_phases(const Dev<R>& d, const BroadAr
     b.bitems[b.bstart[hh] + atomicAdd(&b.bcount[hh], 1)] = s;
   }
   g.sync();
-  for (int s = tid; s < b.S; s += nth)
-    b.rowptr[s] = (s >= b.r0 && s < b.r1) ? bp_row<false>(d, b, ss, s, cutoff2, 0) : 0;
+  // BP_LANES lanes per row; whole warps iterate together (shuffles in bp_row)
+  const int lane = threadIdx.x & 31;
+  const long long nrl = (long long)b.S * BP_LANES;
+  for (long long t0 = tid - lane; t0 < nrl; t0 += nth) {
+    const long long t = t0 + lane;
+    const int s = (int)(t / BP_LANES), c = (int)(t % BP_LANES);
+    const bool act = t < nrl && s >= b.r0 && s < b.r1;
+    const int n = bp_row<false>(d, b, ss, s, act, c, cutoff2, 0);
+    if (t < nrl && c == 0) b.rowptr[s] = act ? n : 0;
+  }
   g.sync();
   if (blockIdx.x == 0) {
     cta_exscan(b.rowptr, b.S);
@@ -1353,8 +1392,12 @@ __device__ __forceinline__ void broadphase_phases(const Dev<R>& d, const BroadAr
     }
   }
   g.sync();
-  for (int s = tid; s < b.S; s += nth)
-    if (s >= b.r0 && s < b.r1) bp_row<true>(d, b, ss, s, cutoff2, b.rowptr[s]);
+  for (long long t0 = tid - lane; t0 < nrl; t0 += nth) {
+    const long long t = t0 + lane;
+    const int s = (int)(t / BP_LANES), c = (int)(t % BP_LANES);
+    const bool act = t < nrl && s >= b.r0 && s < b.r1;
+    bp_row<true>(d, b, ss, s, act, c, cutoff2, act ? b.rowptr[s] : 0);
+  }
 }
 template <class R>
 __global__ void __launch_bounds__(1024, 1) k_broadphase(Dev<R> d, BroadArgs b, const typename VT<R>::R4* ss,
@@ -1366,9 +1409,8 @@ __global__ void __launch_bounds__(1024, 1) k_broadphase(Dev<R> d, BroadArgs b, c
 
 // ------------------------------------------------------------------ contact
 // Penalty law of reading R16: F_on_a = max(0, k_c q - c_c v_n) n,
-// q = r_a + r_b - |D_a - D_b|; partners summed in ascending surface index
-// (= ascending box id).  Rows [r0, r1) are one slab's segment; the load goes
-// to that slab's cf at the voxel's local id.
+// q = r_a + r_b - |D_a - D_b|.  Rows [r0, r1) are one slab's segment; the load
+// goes to that slab's cf at the voxel's local id.
 // Contact loads of surface row s (row a7): the pair law over its CSR partners.
 // CONTACT_LANES lanes share a row: lane c takes partners c, c + L, c + 2L, ...
 // of the ascending partner list, and the L partial sums are combined by a fixed
