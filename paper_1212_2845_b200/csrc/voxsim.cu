@@ -6,6 +6,7 @@
 #include "voxsim.h"
 #include "vx_kernels.cuh"
 #include "vx_topology.cuh"
+#include "vx_fused_yz.cuh"
 
 #include <cub/device/device_scan.cuh>
 
@@ -170,7 +171,9 @@ struct vx_lattice {
   int engine_req = VX_ENGINE_AUTO;        // requested (vx_set_engine); AUTO resolves at the first step
   bool engine_resolved = false;
   bool fused_smem_set[2] = {false, false};
+  bool fused_yz_smem_set[2] = {false, false};
   bool tma_ok = false;                    // TMA-staged fused variant (VX_FUSED_TMA=1; measured slower)
+  bool yz_ok = true;                      // (y, z)-mapped fused pass for nz < 64 (VX_FUSED_YZ)
   int fused_ty = 8;                       // rows per fused block (VX_FUSED_TY overrides)
   int fused_waves = 4;                    // block waves per fused launch (VX_FUSED_WAVES)
   int fused_tune = 1;                     // time candidate segment lengths once (VX_FUSED_TUNE)
@@ -742,6 +745,42 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
   // tuned for this range, or the defaults
   const auto tuned = h->geo_tuned.find(fused_key(s, x_begin, x_end));
   const bool have = tuned != h->geo_tuned.end() && tuned->second.first > 0;
+  if (h->yz_ok && !tma && h->nz < 64 && h->ny >= 2) {
+    // shallow lattice: G rows side by side (vx_fused_yz.cuh); "TY" counts steps of G rows
+    const int G = std::min(h->ny, 256 / h->nz);
+    const int nthr = ((G * h->nz + 31) / 32) * 32;
+    const int mult = ty_force > 0 ? ty_force : (have ? tuned->second.first : h->fused_ty);
+    a.ty = std::min(h->ny, G * std::max(1, mult));
+    a.zchunks = G;
+    a.ntiles_y = (h->ny + a.ty - 1) / a.ty;
+    const int planes = a.p1 - a.p0;
+    const int target = 148 * 2 * h->fused_waves;
+    const int nseg = std::max(1, std::min(planes, (target + a.ntiles_y - 1) / a.ntiles_y));
+    a.sx = (planes + nseg - 1) / nseg;
+    if (sx_force > 0) a.sx = std::min(sx_force, planes);
+    else if (have) a.sx = std::min(tuned->second.second, planes);
+    else if (h->fused_sx > 0) a.sx = std::min(h->fused_sx, planes);
+    const int segs = (planes + a.sx - 1) / a.sx;
+    const int pi = sizeof(R) == 4 ? 0 : 1;
+    if (!h->fused_yz_smem_set[pi]) {
+      VX_CUDA(cudaFuncSetAttribute(k_step_fused_yz<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      VX_CUDA(cudaFuncSetAttribute(k_step_fused_yz<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      h->fused_yz_smem_set[pi] = true;
+    }
+    a.nblk0 = a.ntiles_y * segs;
+    a.p0b = a.p1b = 0;
+    int segs2 = 0;
+    if (x_end2 > x_begin2) {
+      a.p0b = x_begin2 - s.xl0;
+      a.p1b = x_end2 - s.xl0;
+      segs2 = (a.p1b - a.p0b + a.sx - 1) / a.sx;
+    }
+    const unsigned grid = (unsigned)(a.ntiles_y * (segs + segs2));
+    const size_t smem = fused_yz_smem<R>(a.ty, h->nz, G);
+    if (col) k_step_fused_yz<R, true><<<grid, nthr, smem, st>>>(d, a);
+    else k_step_fused_yz<R, false><<<grid, nthr, smem, st>>>(d, a);
+    return VX_OK;
+  }
   int ty = std::min(ty_force > 0 ? ty_force : (have ? tuned->second.first : h->fused_ty), h->ny);
   if (tma)
     while (ty > 1 && fused_tma_smem<R>(ty, threads) > 110 * 1024) --ty;
@@ -1273,6 +1312,7 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   // NCCL inside CUDA graphs
   if (desc->nranks == 1 && desc->nccl_id && std::getenv("VX_FORCE_NCCL")) h->force_nccl = true;
   if (const char* e = std::getenv("VX_FUSED_TMA")) h->tma_ok = std::atoi(e) != 0;
+  if (const char* e = std::getenv("VX_FUSED_YZ")) h->yz_ok = std::atoi(e) != 0;
   if (const char* e = std::getenv("VX_FUSED_TY")) {
     h->fused_ty = std::max(1, std::min(64, std::atoi(e)));
     h->fused_tune = 0;   // an explicit geometry is not tuned away
