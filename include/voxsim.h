@@ -225,8 +225,8 @@ int32_t vx_launches_per_step(const vx_lattice* h);
  * reported in slot [1].
  * VX_ENGINE_AUTO (the default): resolved once, at the first vx_step, to the
  * faster of the two for this lattice -- fused when nz >= 64 and the lattice
- * has >= 2^22 cells, or when it is split into slabs (then fused iff nz >= 32,
- * the same choice on every rank);
+ * has >= 2^22 cells, or when it is split into slabs (then fused unless a
+ * plane has fewer than 32 cells, the same choice on every rank);
  * otherwise both are timed on the current state (as CUDA graphs, without
  * advancing it) and the faster kept.  vx_get_engine returns VX_ENGINE_AUTO
  * until it is resolved, then the engine in use.  Errors: INVALID_ARG for any

@@ -1054,7 +1054,8 @@ vx_status sync_state_copies(vx_lattice* h);
 // VX_ENGINE_AUTO: pick the faster engine for this lattice once, at the first
 // step.  Large lattices with full warps in z (nz >= 64, >= 4M cells) and
 // slab-split lattices (every rank must pick the same engine, so no timing)
-// take the fused engine when nz >= 32 (the design point: C5 1.24 vs 2.33 ms);
+// take the fused engine unless a plane has < 32 cells (C5 1.24 vs 2.33 ms;
+// shallow lattices run the (y, z)-mapped fused pass);
 // otherwise both engines
 // are timed as CUDA graphs of the same 8 steps' kernels -- the fused pass after
 // its geometry tuning, the two-pass kernels on the spare state copy (K4 updates
@@ -1067,7 +1068,7 @@ template <class R> vx_status resolve_engine(vx_lattice* h) {
   h->engine_resolved = true;
   h->clear_graphs();
   if (h->emulated || h->nccl() || (h->nz >= 64 && h->nbox >= (1LL << 22))) {
-    h->engine = h->nz >= 32 ? VX_ENGINE_FUSED : VX_ENGINE_TWO_PASS;
+    h->engine = (long long)h->ny * h->nz >= 32 ? VX_ENGINE_FUSED : VX_ENGINE_TWO_PASS;
     return prepare(h);   // bond records of the two-pass engine
   }
   const bool col = h->collide();
