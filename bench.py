@@ -232,6 +232,7 @@ def run_ours(args):
         nid = vd.bootstrap_nccl_id(dist, rank)
 
     sc = scene_for(args.config, args.precision)
+    replicas = world > 1 and (args.config != "C5" or args.batch > 1)
     # "auto": the library's choice (VX_ENGINE_AUTO, resolved at the first step)
     if args.batch > 1:   # K copies of the scene packed along x, one launch per step (f2)
         from paper_1212_2845_b200.batch import pack
@@ -239,8 +240,12 @@ def run_ours(args):
                   device=local, z_stack=args.z_stack if args.z_stack == "auto" else int(args.z_stack))
         lat = bt.lattice
     else:
-        lat = from_scene(sc, precision=args.precision, device=local, rank=rank, nranks=world,
-                         nccl_id=nid, init_state=sc.v0 is not None, engine=args.engine)
+        # C5 shards into x-slabs; C1-C4 are too small to shard and run as one
+        # replica per GPU
+        shard = world > 1 and not replicas
+        lat = from_scene(sc, precision=args.precision, device=local, rank=rank if shard else 0,
+                         nranks=world if shard else 1, nccl_id=nid if shard else None,
+                         init_state=sc.v0 is not None, engine=args.engine)
     N = lat.num_voxels
     st_init = lat.read_state() if args.batch > 1 and not args.no_e2e else None
     stream = torch.cuda.ExternalStream(lat.stream, device=torch.device("cuda", local))
@@ -281,11 +286,11 @@ def run_ours(args):
     n_instr = max(1, round(kt["all"][1] / max(lat.launches_per_step, 1)))   # measured steps
     lat.set_instrumentation(False)
     ms_max = vd.max_over_ranks([ms], dist if world > 1 else None, "cuda")[0]
-    value = N * args.steps / (ms_max / 1e3)
+    value = N * args.steps / (ms_max / 1e3) * (world if replicas else 1)   # whole job
 
     # ---- roofline of the dominant kernel (live CUDA-event durations)
     x0, x1 = lat.owned_planes()
-    vox_rank = N if world == 1 else N * (x1 - x0) / sc.cells.shape[2]   # dense: per rank
+    vox_rank = N if (world == 1 or replicas) else N * (x1 - x0) / sc.cells.shape[2]   # dense: per rank
     alg = ALG_BYTES[args.precision]
     fused = lat.engine == "fused"
     kinds = ("fused",) if fused else ("bonds", "integrate")
@@ -355,7 +360,7 @@ def run_ours(args):
         ems = max(vd.max_over_ranks([ems, tw * 1e3], dist if world > 1 else None, "cuda"))
         bi = sum(a.nbytes for a in hin)
         bo = sum(a.nbytes for a in (hout.pos, hout.quat, hout.linmom, hout.angmom, hout.latch))
-        e2e = {"value": N * K / (ems / 1e3), "unit": UNIT,
+        e2e = {"value": N * K / (ems / 1e3) * (world if replicas else 1), "unit": UNIT,
                "h2d_bytes_per_step": bi / K, "d2h_bytes_per_step": bo / K,
                "episode": f"set_state (H2D) + {K} steps + read_state (D2H) per episode; "
                           "bytes per step = episode bytes / K"}
@@ -373,7 +378,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak" if replicas else "strong", "vs_baseline": None,
             "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
             "config": {"workload": (f"{args.batch} x " if args.batch > 1 else "") +
                                    f"{sc.name} ({sc.cells.shape[2]}x{sc.cells.shape[1]}x"
@@ -383,7 +388,7 @@ def run_ours(args):
                           if args.batch > 1 else {}),
                        "timing": "per-kernel CUDA events in the timed region" if live else
                                  "CUDA graphs; kernel breakdown from a separate instrumented pass",
-                       "parallelism": f"x-slab{world}",
+                       "parallelism": f"replicas{world}" if replicas else f"x-slab{world}",
                        "l2": "no flush: working set (state + bond records) >> 126 MB L2"
                              if N > 1_000_000 else "small lattice, L2-resident"},
             "clocks": clocks, "gpu_launches": lat.launches_per_step * args.steps * world,
