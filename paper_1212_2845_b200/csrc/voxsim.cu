@@ -546,7 +546,7 @@ vx_status setup_collision(vx_lattice* h) {
     VX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &per_sm, h->prec == 32 ? (const void*)k_broadphase<float> : (const void*)k_broadphase<double>, 1024, 0));
     VX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    h->bp_grid = std::max(1, std::min(std::max(1, per_sm) * sms, (std::max(S, H) + 1023) / 1024));
+    h->bp_grid = std::max(1, std::min(std::max(1, per_sm) * sms, (std::max(S * BP_LANES, H) + 1023) / 1024));
   }
   const int rows = h->rows_end() - h->rows_begin();
   h->cap = std::max<long long>(1 << 16, 128LL * rows);
