@@ -158,6 +158,15 @@ vx_status vx_load_checkpoint(vx_lattice* h, const void* buf, int64_t bytes);
 /* Set the step counter n (time t_n = n dt of the temperature schedule). */
 vx_status vx_set_step(vx_lattice* h, int64_t n);
 
+/* Build, without running them, the CUDA graphs vx_step(h, n) will replay from
+ * the current state (and resolve VX_ENGINE_AUTO, tune the launch geometry,
+ * pack the surface table): the state does not advance.  Optional -- vx_step
+ * does the same on first use; calling this first keeps graph construction out
+ * of a timed region.  Graphs depend on n modulo 32 steps, the state-copy parity
+ * and the instrumentation setting, so call it after vx_set_instrumentation.
+ * Errors: INVALID_ARG for n < 0; STATE before materials/environment are set. */
+vx_status vx_prepare_steps(vx_lattice* h, int64_t n);
+
 /* Advance n steps (n >= 0) of the synchronous two-phase update:
  * bond loads from the frozen state (Eq. 13-24, 33-35, 39-40), per-voxel
  * fixed-order sums (Eq. 25-26), gravity, ground damping, self collision,

@@ -66,6 +66,7 @@ SIGNATURES = {
     "vx_save_checkpoint": (_I32, [_P, _P, _I64]),
     "vx_load_checkpoint": (_I32, [_P, _P, _I64]),
     "vx_step": (_I32, [_P, _I64]),
+    "vx_prepare_steps": (_I32, [_P, _I64]),
     "vx_read_state": (_I32, [_P, _P, _P, _P, _P, _P]),
     "vx_read_voxels": (_I32, [_P, _P, _I64, _P, _P, _P, _P, _P]),
     "vx_dt": (_D, [_P]),

@@ -1134,52 +1134,91 @@ template <class R> vx_status resolve_engine(vx_lattice* h) {
   return VX_OK;
 }
 
-template <class R> vx_status run_steps(vx_lattice* h, long long n) {
+// CUDA graphs of G steps; the remainder is captured as its own graph.  The
+// fused engine ping-pongs two state copies, so a graph also depends on which
+// copy is current when it starts (key = 2 g + parity).  With instrumentation
+// on, the graphs carry event-record nodes around every launch class of every
+// instr_stride-th step (their own cache); two event pools alternate between
+// graph replays, so a chunk's times are read while the next chunk runs.
+constexpr long long kGraphSteps = 32;
+
+// The graph of g steps starting at state-copy parity `par`, event pool `pool`
+// (captured and instantiated on first use).
+template <class R>
+vx_status get_graph(vx_lattice* h, long long g, int par, int pool, cudaGraphExec_t* out) {
+  const long long G = kGraphSteps;
+  const long long key = 2 * g + (h->fused() ? par : 0) +
+                        (h->instr ? ((long long)h->instr_stride << 40) + ((long long)pool << 39) : 0);
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end()) {
+    const int par0 = h->slabs[0].par;
+    for (auto& s : h->slabs) s.par = par;
+    cudaGraph_t graph;
+    VX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    vx_status st = VX_OK;
+    for (long long s = 0; s < g && st == VX_OK; ++s) {
+      cudaEvent_t* ev = nullptr;
+      if (h->instr && s % h->instr_stride == 0) ev = &h->events[(size_t)pool * G * 4 + (size_t)s * 4];
+      st = enqueue_step<R>(h, ev);
+    }
+    cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+    for (auto& s : h->slabs) s.par = par0;   // capture only recorded the flips
+    if (st != VX_OK) return st;
+    if (ce != cudaSuccess) return fail(VX_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    cudaGraphExec_t ex;
+    VX_CUDA(cudaGraphInstantiate(&ex, graph, 0));
+    cudaGraphDestroy(graph);
+    VX_CUDA(cudaGraphUpload(ex, h->stream));
+    it = h->graphs.emplace(key, ex).first;
+  }
+  *out = it->second;
+  return VX_OK;
+}
+
+// Everything a run of n steps needs before its first launch: the engine, the
+// launch geometry, the surface table, the event pools.
+template <class R> vx_status ready_steps(vx_lattice* h) {
   VX_TRY(resolve_engine<R>(h));
   VX_TRY(tune_fused<R>(h));
   if (h->collide() && h->ss_dirty) VX_TRY(pack_surface<R>(h));
-  // CUDA graphs of G steps; the remainder is captured as its own graph.  The
-  // fused engine ping-pongs two state copies, so a graph also depends on which
-  // copy is current when it starts (key = 2 g + parity).  With instrumentation
-  // on, the graphs carry event-record nodes around every launch class of every
-  // instr_stride-th step (their own cache); two event pools alternate between
-  // graph replays, so a chunk's times are read while the next chunk runs.
-  const long long G = 32;
   if (h->instr) {
-    while (h->events.size() < (size_t)G * 8) {
+    while (h->events.size() < (size_t)kGraphSteps * 8) {
       cudaEvent_t e;
       VX_CUDA(cudaEventCreate(&e));
       h->events.push_back(e);
     }
   }
+  return VX_OK;
+}
+
+// The graphs vx_step(n) will replay, built without running them.
+template <class R> vx_status prepare_graphs(vx_lattice* h, long long n) {
+  VX_TRY(ready_steps<R>(h));
+  long long left = n;
+  int pool = 0, par = h->slabs[0].par;
+  while (left > 0) {
+    const long long g = left >= kGraphSteps ? kGraphSteps : left;
+    cudaGraphExec_t ex;
+    VX_TRY(get_graph<R>(h, g, par, pool, &ex));
+    if (h->fused() && (g & 1)) par ^= 1;
+    left -= g;
+    if (h->instr) pool ^= 1;
+  }
+  VX_CUDA(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+template <class R> vx_status run_steps(vx_lattice* h, long long n) {
+  VX_TRY(ready_steps<R>(h));
+  const long long G = kGraphSteps;
   long long left = n;
   int pool = 0;
   long long pending = 0;   // steps of the chunk in flight whose times are unread
   while (left > 0) {
     const long long g = left >= G ? G : left;
-    const int par = h->slabs[0].par;
-    const long long key = 2 * g + (h->fused() ? par : 0) +
-                          (h->instr ? ((long long)h->instr_stride << 40) + ((long long)pool << 39) : 0);
-    auto it = h->graphs.find(key);
-    if (it == h->graphs.end()) {
-      cudaGraph_t graph;
-      VX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-      vx_status st = VX_OK;
-      for (long long s = 0; s < g && st == VX_OK; ++s) {
-        cudaEvent_t* ev = nullptr;
-        if (h->instr && s % h->instr_stride == 0) ev = &h->events[(size_t)pool * G * 4 + (size_t)s * 4];
-        st = enqueue_step<R>(h, ev);
-      }
-      cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
-      for (auto& s : h->slabs) s.par = par;   // capture only recorded the flips
-      if (st != VX_OK) return st;
-      if (ce != cudaSuccess) return fail(VX_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-      cudaGraphExec_t ex;
-      VX_CUDA(cudaGraphInstantiate(&ex, graph, 0));
-      cudaGraphDestroy(graph);
-      it = h->graphs.emplace(key, ex).first;
-    }
-    VX_CUDA(cudaGraphLaunch(it->second, h->stream));
+    cudaGraphExec_t ex;
+    VX_TRY(get_graph<R>(h, g, h->slabs[0].par, pool, &ex));
+    VX_CUDA(cudaGraphLaunch(ex, h->stream));
     if (h->fused() && (g & 1)) h->flip();
     left -= g;
     if (h->instr) {
@@ -1616,6 +1655,16 @@ vx_status vx_set_step(vx_lattice* h, int64_t n) {
   VX_CUDA(cudaMemcpy(&c->next, &v, 8, cudaMemcpyHostToDevice));
   h->steps_done = n;
   return VX_OK;
+}
+
+vx_status vx_prepare_steps(vx_lattice* h, int64_t n) {
+  if (!h || n < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
+  if (n == 0) return VX_OK;
+  VX_TRY(set_device(h));
+  VX_TRY(prepare(h));
+  if (h->N == 0) return VX_OK;
+  if (h->prec == 32) return prepare_graphs<float>(h, n);
+  return prepare_graphs<double>(h, n);
 }
 
 vx_status vx_step(vx_lattice* h, int64_t n) {

@@ -149,6 +149,10 @@ class Lattice:
         _check(N.load().vx_set_step(self._h, int(n)))
 
     # ------------------------------------------------------------ stepping
+    def prepare_steps(self, n):
+        """Build the CUDA graphs step(n) will replay, without advancing the state."""
+        _check(N.load().vx_prepare_steps(self._h, int(n)))
+
     def step(self, n=1):
         _check(N.load().vx_step(self._h, int(n)))
 

@@ -67,3 +67,18 @@ def test_auto_can_be_requested_again():
     assert a.engine in ("fused", "two_pass")
     with pytest.raises(Exception):
         a.set_engine(7)
+
+
+@pytest.mark.parametrize("name", ["C2c", "sphere"])
+def test_prepare_steps_does_not_advance(name):
+    sc = {"C2c": W.get("C2c"), "sphere": _sphere()}[name]
+    a = from_scene(sc, precision=32)
+    a.step(3)
+    s0 = _flat(a.read_state())
+    a.prepare_steps(77)                 # engine resolved, graphs built, nothing run
+    assert a.engine in ("fused", "two_pass")
+    assert np.array_equal(_flat(a.read_state()), s0) and a.steps_done == 3
+    a.step(77)
+    b = from_scene(sc, precision=32, engine=a.engine)
+    b.step(80)
+    assert np.array_equal(_flat(a.read_state()), _flat(b.read_state()))
