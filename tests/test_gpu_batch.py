@@ -81,11 +81,3 @@ def test_batch_rejects_filled_separator_layer():
         lat.set_batch_z(2)
     lat.set_batch_z(0)
 
-
-def test_batch_z_stack_layout():
-    from paper_1212_2845_b200.batch import z_stack_for
-    assert z_stack_for(4096, 1) == 128          # 255 layers of cantilevers
-    assert z_stack_for(64, 20) == 11            # 6 x blocks of 11 cubes (64 scenes)
-    assert z_stack_for(32, 16) == 11            # 3 x blocks of 11 walkers
-    assert z_stack_for(100, 40) == 1            # deep scenes: x only
-    assert z_stack_for(1, 5) == 1
