@@ -386,7 +386,8 @@ def run_ours(args):
                                    f"{sc.name} ({sc.cells.shape[2]}x{sc.cells.shape[1]}x"
                                    f"{sc.cells.shape[0]}, {N} voxels, {lat.num_bonds} bonds)",
                        "engine": lat.engine,
-                       **({"packing": f"{-(-args.batch // bt.z_stack)} x-blocks x {bt.z_stack} z-blocks"}
+                       **({"packing": f"{-(-args.batch // (bt.z_stack * bt.y_stack))} x-blocks x "
+                                      f"{bt.y_stack} y-blocks x {bt.z_stack} z-blocks"}
                           if args.batch > 1 else {}),
                        "timing": "per-kernel CUDA events in the timed region" if live else
                                  "CUDA graphs; kernel breakdown from a separate instrumented pass",

@@ -259,8 +259,15 @@ vx_status vx_set_batch(vx_lattice* h, int32_t stride);
  * block (k mod stride), so each scene sees what it would alone; self collision
  * ignores pairs of different z blocks.  stride 0 = no z stacking.  Errors:
  * INVALID_ARG if a separator layer is not empty.  vx_num_scenes counts x
- * blocks times z blocks. */
+ * blocks times y blocks times z blocks. */
 vx_status vx_set_batch_z(vx_lattice* h, int32_t stride);
+/* Scenes stacked along y as well: every `stride` rows one scene, row stride-1
+ * of each block empty.  The physics is invariant under a y translation; self
+ * collision ignores pairs of different y blocks.  For scenes whose y-z plane
+ * is smaller than a warp (ny * nz < 32, e.g. a 10 x 1 x 1 cantilever) y
+ * stacking gives the (y, z)-mapped fused pass full warps.  stride 0 = none.
+ * Errors: INVALID_ARG if a separator row is not empty. */
+vx_status vx_set_batch_y(vx_lattice* h, int32_t stride);
 int32_t vx_num_scenes(const vx_lattice* h);
 vx_status vx_set_engine(vx_lattice* h, int32_t engine);
 int32_t vx_get_engine(const vx_lattice* h);

@@ -85,6 +85,7 @@ SIGNATURES = {
     "vx_set_engine": (_I32, [_P, _I32]),
     "vx_set_batch": (_I32, [_P, _I32]),
     "vx_set_batch_z": (_I32, [_P, _I32]),
+    "vx_set_batch_y": (_I32, [_P, _I32]),
     "vx_num_scenes": (_I32, [_P]),
     "vx_get_engine": (_I32, [_P]),
     "vx_destroy": (None, [_P]),

@@ -181,6 +181,7 @@ struct vx_lattice {
   std::map<long long, std::pair<int, int>> geo_tuned;   // (TY, SX) chosen per launch range
   int batch_stride = 0;                   // planes per batched scene (vx_set_batch)
   int batch_stride_z = 0;                 // layers per z-stacked scene (vx_set_batch_z)
+  int batch_stride_y = 0;                 // rows per y-stacked scene (vx_set_batch_y)
 
   bool fused() const { return engine == VX_ENGINE_FUSED; }
   void flip() {
@@ -935,7 +936,7 @@ template <class R> vx_status enqueue_step(vx_lattice* h, cudaEvent_t* ev) {
     BroadArgs b{gb, S, h->rows_begin(), h->rows_end(), h->cellh.as<int4>(),
                 h->bcount.as<int>(), h->bstart.as<int>(), h->bitems.as<int>(),
                 h->rowptr.as<int>(), h->col.as<int>(), h->cap, h->H, h->clk.as<Clock>(),
-                h->batch_stride, h->batch_stride_z, h->sijk.as<int4>()};
+                h->batch_stride, h->batch_stride_z, h->batch_stride_y, h->sijk.as<int4>()};
     const double hc = h->cutoff * 1.001;
     {   // cooperative: all CTAs resident (grid-wide barriers between the phases)
       Dev<R> d0 = make_dev<R>(h, h->slabs[0]);
@@ -1911,11 +1912,28 @@ vx_status vx_set_batch_z(vx_lattice* h, int32_t stride) {
   VX_TRY(set_device(h));
   return set_force_rebuild(h);
 }
+vx_status vx_set_batch_y(vx_lattice* h, int32_t stride) {
+  if (!h || stride < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
+  if (stride > 0) {
+    if (stride < 2) return fail(VX_ERR_INVALID_ARG, "a y-stacked scene needs >= 1 row + a separator");
+    // every stride-th row (stride-1, 2 stride-1, ...) must be empty
+    for (int y = stride - 1; y < h->ny; y += stride)
+      for (int z = 0; z < h->nz; ++z)
+        for (int x = 0; x < h->nx; ++x)
+          if (h->cells[(size_t)x + (size_t)h->nx * ((size_t)y + (size_t)h->ny * z)])
+            return fail(VX_ERR_INVALID_ARG, "separator row y=" + std::to_string(y) + " is not empty");
+  }
+  h->batch_stride_y = stride;
+  h->clear_graphs();
+  VX_TRY(set_device(h));
+  return set_force_rebuild(h);
+}
 int32_t vx_num_scenes(const vx_lattice* h) {
   if (!h) return -1;
   const int kx = h->batch_stride ? (h->nx + h->batch_stride - 1) / h->batch_stride : 1;
+  const int ky = h->batch_stride_y ? (h->ny + h->batch_stride_y - 1) / h->batch_stride_y : 1;
   const int kz = h->batch_stride_z ? (h->nz + h->batch_stride_z - 1) / h->batch_stride_z : 1;
-  return kx * kz;
+  return kx * ky * kz;
 }
 
 vx_status vx_set_engine(vx_lattice* h, int32_t engine) {

@@ -1216,6 +1216,7 @@ struct BroadArgs {
   Clock* clk;
   int batch_stride;       // planes per batched scene (0: one scene); no cross-scene pairs
   int batch_stride_z;     // layers per z-stacked batched scene (0: none)
+  int batch_stride_y;     // rows per y-stacked batched scene (0: none)
   const int4* sijk;       // S lattice coordinates (i, j, k) of the surface entries
 };
 
@@ -1295,6 +1296,7 @@ __device__ __forceinline__ int bp_row(const Dev<R>& d, const BroadArgs& b,
         if (abs(a.x - o.x) + abs(a.y - o.y) + abs(a.z - o.z) <= 3) continue;
         if (b.batch_stride && a.x / b.batch_stride != o.x / b.batch_stride) continue;
         if (b.batch_stride_z && a.z / b.batch_stride_z != o.z / b.batch_stride_z) continue;
+        if (b.batch_stride_y && a.y / b.batch_stride_y != o.y / b.batch_stride_y) continue;
         const R4 pb = ss[2 * u];
         const R rx = d.l * (R)(a.x - o.x) + (pa.x - pb.x);
         const R ry = d.l * (R)(a.y - o.y) + (pa.y - pb.y);

@@ -237,6 +237,10 @@ class Lattice:
         """Declare K scenes packed along x, `stride` planes each (incl. separator)."""
         _check(N.load().vx_set_batch(self._h, int(stride)))
 
+    def set_batch_y(self, stride):
+        """Declare scenes stacked along y as well, `stride` rows each (incl. separator)."""
+        _check(N.load().vx_set_batch_y(self._h, int(stride)))
+
     def set_batch_z(self, stride):
         """Declare scenes stacked along z as well, `stride` layers each (incl. separator)."""
         _check(N.load().vx_set_batch_z(self._h, int(stride)))

@@ -81,3 +81,28 @@ def test_batch_rejects_filled_separator_layer():
         lat.set_batch_z(2)
     lat.set_batch_z(0)
 
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_batch_y_stacked_cantilevers_equal_alone(prec):
+    # 10 x 1 x 1 cantilevers (a fixed end, a tip load, ground damping) stacked
+    # along y: every scene evolves as alone
+    scenes = [W.cantilever(force=f) for f in (1e-3, 2e-3, 5e-4, 1.5e-3, 3e-3, 1e-4, 2.5e-3)]
+    b = pack(scenes, precision=prec, engine="fused")
+    assert b.y_stack == 7 and b.lattice.num_scenes == 7
+    b.lattice.step(400)
+    st = b.lattice.read_state()
+    for s, sc in enumerate(scenes):
+        lat = from_scene(sc, precision=prec, engine="fused")
+        lat.step(400)
+        u_ref = lat.read_state().pos - sc.initial_state()[0]
+        u = b.displacement_of(s, st)
+        assert np.abs(u - u_ref).max() <= (1e-12 if prec == 64 else 1e-5) * np.abs(u_ref).max(), s
+
+
+def test_batch_rejects_filled_separator_row():
+    sc = W.cube(n=4)
+    lat = from_scene(sc, precision=32)
+    with pytest.raises(VoxError):
+        lat.set_batch_y(2)
+    lat.set_batch_y(0)
