@@ -3,6 +3,8 @@ forced voxels, floor / gravity / temperature / self collision on or off --
 the CUDA path (both engines, fp64) against the oracle after 150 steps, and the
 fp32 fused path within the fp32 bar.  Catches edge cases the named configs
 do not reach."""
+import os
+
 import numpy as np
 import pytest
 
@@ -10,6 +12,7 @@ import workloads as W
 from parity import errors, run_pair
 
 pytestmark = pytest.mark.gpu
+SEEDS = range(int(os.environ.get("VX_FUZZ_SEEDS", "30")))   # more for an extended run
 
 
 def _scene(seed):
@@ -38,7 +41,7 @@ def _scene(seed):
     return sc
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", SEEDS)
 @pytest.mark.parametrize("engine", ["fused", "two_pass"])
 def test_fuzz_fp64(seed, engine):
     sc = _scene(seed)
@@ -48,7 +51,7 @@ def test_fuzz_fp64(seed, engine):
     assert np.array_equal(g.latch, o.latch)
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", SEEDS)
 def test_fuzz_fp32_fused(seed):
     sc = _scene(seed)
     g, o, p0, lat, orc = run_pair(sc, 150, 32, engine="fused")
@@ -56,7 +59,7 @@ def test_fuzz_fp32_fused(seed):
     assert e["eD"] <= 1e-4, (seed, e, sc.cells.shape)
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", SEEDS)
 def test_fuzz_slabs_and_geometry_bitwise(seed):
     """The same random scenes on P emulated slabs and under the tuned geometry:
     bitwise equal to one domain (fp32, both engines)."""
