@@ -1094,11 +1094,11 @@ template <class R> vx_status resolve_engine(vx_lattice* h) {
     const cudaError_t ie = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (ie != cudaSuccess) return fail(VX_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
-    cudaGraphLaunch(ex, h->stream);
-    cudaEventRecord(ev0.e, h->stream);
-    for (int r = 0; r < 4; ++r) cudaGraphLaunch(ex, h->stream);
-    cudaEventRecord(ev1.e, h->stream);
-    const cudaError_t se = cudaEventSynchronize(ev1.e);
+    cudaError_t se = cudaGraphLaunch(ex, h->stream);
+    if (se == cudaSuccess) se = cudaEventRecord(ev0.e, h->stream);
+    for (int r = 0; r < 4 && se == cudaSuccess; ++r) se = cudaGraphLaunch(ex, h->stream);
+    if (se == cudaSuccess) se = cudaEventRecord(ev1.e, h->stream);
+    if (se == cudaSuccess) se = cudaEventSynchronize(ev1.e);
     cudaGraphExecDestroy(ex);
     if (se != cudaSuccess) return fail(VX_ERR_CUDA, std::string("engine timing: ") + cudaGetErrorString(se));
     VX_CUDA(cudaEventElapsedTime(ms, ev0.e, ev1.e));
