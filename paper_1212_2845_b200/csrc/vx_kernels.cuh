@@ -1309,7 +1309,7 @@ __device__ __forceinline__ int bp_row(const Dev<R>& d, const BroadArgs& b,
     return n;
   };
   const int lane = threadIdx.x & 31, g0 = lane & ~(BP_LANES - 1);
-  const unsigned gm = ((1u << BP_LANES) - 1u) << g0;   // this row's lanes
+  const unsigned gm = BP_LANES == 32 ? 0xffffffffu : (((1u << (BP_LANES & 31)) - 1u) << g0);   // this row's lanes
   cnt = scan(false, 0);
   if (!FILL) {
 #pragma unroll
