@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define VOXSIM_ABI_VERSION 1
+#define VOXSIM_ABI_VERSION 2   /* 2: vx_prepare_steps, vx_set_batch_y/_z, VX_ENGINE_AUTO default */
 
 typedef struct vx_lattice vx_lattice; /* opaque, library-owned */
 

@@ -98,6 +98,9 @@ SIGNATURES = {
 _lib = None
 
 
+ABI_VERSION = 2   # include/voxsim.h VOXSIM_ABI_VERSION
+
+
 def load():
     """Load libvoxsim.so (raises if it has not been built)."""
     global _lib
@@ -110,5 +113,8 @@ def load():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        if L.vx_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {L.vx_abi_version()}, this binding needs "
+                              f"{ABI_VERSION}: rebuild with `python -m paper_1212_2845_b200.build`")
         _lib = L
     return _lib
