@@ -274,7 +274,7 @@ vx_status build_topology(vx_lattice* h) {
   VX_CUDA(cudaMemsetAsync(counts.p, 0, 16, st));
   VX_CUDA(cudaMemsetAsync(pairs.p, 0, 2048 * 4, st));
   VX_CUDA(cudaMemsetAsync(maxc.p, 0, 4, st));
-  k_topo_count<<<topo_grid(nbox), 256, 0, st>>>(cd, nx, ny, nz, nbox, counts.as<unsigned long long>(),
+  k_topo_count<<<std::min(topo_grid(nbox), 148u * 4), 256, 0, st>>>(cd, nx, ny, nz, nbox, counts.as<unsigned long long>(),
                                                 pairs.as<unsigned>(), maxc.as<int>(), flag.as<uint32_t>());
   VX_TRY(exclusive_scan_u32(flag.as<uint32_t>(), scan.as<uint32_t>(), nbox, st));
   unsigned long long cnt[2];
