@@ -30,6 +30,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# tools/oracle_mutants.py points this at a deliberately broken build of
+# oracle.cpp to check that the pins fail (a mutation test of the pins)
+_LIB_OVERRIDE = os.environ.get("VX_ORACLE_LIB")
 
 
 def build(force: bool = False) -> str:
@@ -68,8 +71,11 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(_LIB_PATH)
+        if _LIB_OVERRIDE:
+            L = ctypes.CDLL(_LIB_OVERRIDE)
+        else:
+            build()
+            L = ctypes.CDLL(_LIB_PATH)
         P = ctypes.c_void_p
         dp = ctypes.POINTER(ctypes.c_double)
         L.orc_create.restype = P

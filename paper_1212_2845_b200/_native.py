@@ -109,12 +109,17 @@ def load():
             raise ImportError(f"{LIB_PATH} is missing: build the CUDA extension with "
                               "`python -m paper_1212_2845_b200.build` (there is no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
+        # the ABI version first: a stale library may lack later symbols
+        ver = getattr(L, "vx_abi_version", None)
+        if ver is not None:
+            ver.restype, ver.argtypes = _I32, []
+        have = ver() if ver is not None else None
+        if have != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {have}, this binding needs "
+                              f"{ABI_VERSION}: rebuild with `python -m paper_1212_2845_b200.build`")
         for name, (res, args) in SIGNATURES.items():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
-        if L.vx_abi_version() != ABI_VERSION:
-            raise ImportError(f"{LIB_PATH} has ABI {L.vx_abi_version()}, this binding needs "
-                              f"{ABI_VERSION}: rebuild with `python -m paper_1212_2845_b200.build`")
         _lib = L
     return _lib

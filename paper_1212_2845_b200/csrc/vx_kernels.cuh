@@ -851,6 +851,10 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
     }
   }
 
+  // zrec / edge buffer parity: a row counter carried across planes, so two
+  // consecutive rows never share a buffer even when a tile has an odd number of
+  // rows (the last row of plane i and the first of plane i+1 are adjacent)
+  int rc = 0;
   for (int i = i0; i < i1; ++i) {
     VS<R> va, vb;    // ping-pong: this row's voxel and the next row's
     Rec6<R>& ry = yrec[tk];   // -y slot record of the current row: +y bond of the row below
@@ -950,8 +954,9 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
     for (int j = j0; j < j1; ++j) {
       const uint32_t m = act ? meta_of(va.p.w) : 0u;
       const bool full = __all_sync(0xffffffffu, (m & (M_FILLED | M_FIXED | kXY)) == (M_FILLED | kXY));
-      if (full) row(std::true_type{}, j, va, vb, (j - j0) & 1);
-      else row(std::false_type{}, j, va, vb, (j - j0) & 1);
+      if (full) row(std::true_type{}, j, va, vb, rc & 1);
+      else row(std::false_type{}, j, va, vb, rc & 1);
+      ++rc;
       va = vb;
     }
   }
@@ -1436,7 +1441,9 @@ __global__ void __launch_bounds__(256) k_contact(Dev<R> d, const unsigned* gbox,
     const R4 moa = ss[2 * s + 1];
     const R dT = (R)d.clk->dT;
     const R ra = d.half_l * (R(1) + ma.alpha * dT);
-    const int q1 = rowptr[s + 1];
+    // after a pair-list overflow the row pointers exceed the list (VX_ERR_STATE is
+    // reported at the end of vx_step): never read past it
+    const int q1 = d.clk->overflow ? 0 : rowptr[s + 1];
     for (int q = rowptr[s] + c; q < q1; q += CONTACT_LANES) {
       const int u = col[q];
       const int4 b = sijk[u];

@@ -35,6 +35,25 @@ def _ptr(a):
     return None if a is None else a.ctypes.data
 
 
+def _arr(a, n, cols, dtype, name, out=False):
+    """A C-contiguous array of shape (n, cols) (cols 0: (n,)) and the dtype the
+    C ABI reads or writes; the library copies n * cols elements, so a short or
+    mistyped buffer is refused here rather than overrun there."""
+    if a is None:
+        return None
+    shape = (n,) if cols == 0 else (n, cols)
+    if out:
+        if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous
+                and a.shape == shape):
+            raise ValueError(f"{name}: need a C-contiguous {np.dtype(dtype).name} array of shape "
+                             f"{shape}, got {getattr(a, 'dtype', type(a))} {getattr(a, 'shape', '')}")
+        return a
+    a = np.ascontiguousarray(a, dtype=dtype)
+    if a.shape != shape and not (cols and a.shape == (n * cols,)):
+        raise ValueError(f"{name}: need shape {shape}, got {a.shape}")
+    return a
+
+
 @dataclass
 class State:
     pos: np.ndarray      # (n,3) absolute positions D, m
@@ -117,8 +136,8 @@ class Lattice:
         _check(N.load().vx_set_environment(self._h, ctypes.byref(e)))
 
     def set_boundary(self, fixed=None, f_ext=None):
-        f = None if fixed is None else np.ascontiguousarray(fixed, dtype=np.uint8)
-        x = None if f_ext is None else np.ascontiguousarray(f_ext, dtype=np.float64)
+        f = _arr(fixed, self.n, 0, np.uint8, "fixed")
+        x = _arr(f_ext, self.n, 3, np.float64, "f_ext")
         _check(N.load().vx_set_boundary(self._h, _ptr(f), _ptr(x)))
 
     def add_region(self, kind, origin, size, force=(0.0, 0.0, 0.0)):
@@ -129,9 +148,10 @@ class Lattice:
         _check(N.load().vx_add_region(self._h, int(k), o, s, f))
 
     def set_state(self, pos=None, quat=None, linmom=None, angmom=None, latch=None):
-        arrs = [None if a is None else np.ascontiguousarray(a, dtype=t)
-                for a, t in ((pos, np.float64), (quat, np.float64), (linmom, np.float64),
-                             (angmom, np.float64), (latch, np.uint8))]
+        arrs = [_arr(a, self.n, c, t, nm)
+                for a, c, t, nm in ((pos, 3, np.float64, "pos"), (quat, 4, np.float64, "quat"),
+                                    (linmom, 3, np.float64, "linmom"),
+                                    (angmom, 3, np.float64, "angmom"), (latch, 0, np.uint8, "latch"))]
         _check(N.load().vx_set_state(self._h, *[_ptr(a) for a in arrs]))
 
     def save_checkpoint(self) -> bytes:
@@ -161,6 +181,12 @@ class Lattice:
         if out is None:
             out = State(np.empty((n, 3)), np.empty((n, 4)), np.empty((n, 3)), np.empty((n, 3)),
                         np.empty(n, np.uint8))
+        else:
+            for a, c, t, nm in ((out.pos, 3, np.float64, "pos"), (out.quat, 4, np.float64, "quat"),
+                                (out.linmom, 3, np.float64, "linmom"),
+                                (out.angmom, 3, np.float64, "angmom"),
+                                (out.latch, 0, np.uint8, "latch")):
+                _arr(a, n, c, t, nm, out=True)
         _check(N.load().vx_read_state(self._h, _ptr(out.pos), _ptr(out.quat), _ptr(out.linmom),
                                       _ptr(out.angmom), _ptr(out.latch)))
         return out

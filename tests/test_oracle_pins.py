@@ -478,6 +478,22 @@ def test_contact_excludes_lattice_neighbours_within_manhattan_3():
     assert len(o.contact_pairs()) == 0
 
 
+@pytest.mark.parametrize("n,excluded", [(4, True), (5, False)])
+def test_contact_force_path_excludes_manhattan_3(n, excluded):
+    """The step's contact loads use the same exclusion: a rod whose end
+    voxels overlap steps exactly as without self collision when the ends are
+    Manhattan 3 apart, and differently at Manhattan 4."""
+    runs = []
+    for col in (0, 1):
+        o, s = sim(np.ones((1, 1, n)), [mat()], self_collision=col, zeta_col=0.2)
+        pos, quat, P, phi, latch = s.initial_state()
+        pos[n - 1] = pos[0] + np.array([0.5 * L, 0.1 * L, 0])
+        o.set_state(pos, quat, P, phi, latch)
+        o.step(3)
+        runs.append(o.read_state().linmom)
+    assert np.array_equal(runs[0], runs[1]) == excluded
+
+
 def test_contact_pairs_brute_force_definition():
     rng = np.random.default_rng(5)
     cells = (rng.random((4, 4, 6)) < 0.6).astype(np.uint8)
