@@ -1421,6 +1421,7 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   if ((s = sync_state_copies(h)) != VX_OK) return bail(s);
   Clock c0{};
   c0.err = ~0ULL;
+  c0.fault = ~0ULL;
   c0.force_rebuild = 1;
   if (cudaMemcpy(h->clk.p, &c0, sizeof c0, cudaMemcpyHostToDevice) != cudaSuccess)
     return bail(fail(VX_ERR_CUDA, "upload failed"));
@@ -1639,7 +1640,7 @@ vx_status vx_load_checkpoint(vx_lattice* h, const void* buf, int64_t bytes) {
   std::memcpy(&c, p, sizeof c);
   c.force_rebuild = 1;   // the pair list is rebuilt from the restored state
   c.err = ~0ULL;
-  c.fault = 0;
+  c.fault = ~0ULL;
   c.overflow = 0;
   VX_CUDA(cudaMemcpy(h->clk.p, &c, sizeof c, cudaMemcpyHostToDevice));
   h->steps_done = hd.steps_done;
@@ -1679,22 +1680,23 @@ vx_status vx_step(vx_lattice* h, int64_t n) {
   h->steps_done += n;
   Clock c;
   VX_CUDA(cudaMemcpy(&c, h->clk.p, sizeof c, cudaMemcpyDeviceToHost));
-  unsigned long long err = c.err;
-  int fault = c.fault, overflow = c.overflow;
+  unsigned long long err = c.err, fault = c.fault;
+  int overflow = c.overflow;
   if (h->nccl()) {   // every rank returns the same status
     DevBuf t;
     VX_TRY(t.alloc(24));
-    unsigned long long hv[3] = {err, ~0ULL - (unsigned long long)fault, ~0ULL - (unsigned long long)overflow};
+    unsigned long long hv[3] = {err, fault, ~0ULL - (unsigned long long)overflow};
     VX_CUDA(cudaMemcpy(t.p, hv, 24, cudaMemcpyHostToDevice));
     VX_NCCL(ncclAllReduce(t.p, t.p, 3, ncclUint64, ncclMin, h->comm, h->stream));
     VX_CUDA(cudaMemcpyAsync(hv, t.p, 24, cudaMemcpyDeviceToHost, h->stream));
     VX_CUDA(cudaStreamSynchronize(h->stream));
     err = hv[0];
-    fault = (int)(~0ULL - hv[1]);
+    fault = hv[1];
     overflow = (int)(~0ULL - hv[2]);
   }
   if (overflow) return fail(VX_ERR_STATE, "contact pair list capacity exceeded");
-  if (fault) return fail(VX_ERR_DIVERGED, "non-positive thermal rest length (S:205)");
+  if (fault != ~0ULL)
+    return fail(VX_ERR_DIVERGED, "non-positive thermal rest length at step " + std::to_string(fault) + " (S:205)");
   if (err != ~0ULL) {
     const long long step = (long long)(err >> 32);
     const long long ext = (long long)(err & 0xffffffffULL);

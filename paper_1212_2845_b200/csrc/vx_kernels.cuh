@@ -28,7 +28,7 @@ struct Clock {
   int rebuild;                  // broadphase runs this step
   int force_rebuild;            // set by set_state / set_environment
   unsigned long long err;       // min over ((step << 32) | box id) of diverged voxels
-  int fault;                    // 1: non-positive thermal rest length
+  unsigned long long fault;     // first step with a non-positive thermal rest length (~0: none)
   int overflow;                 // contact pair list capacity exceeded
   long long npairs;             // pairs a<b in the shortlist
   long long rebuilds;
@@ -81,7 +81,8 @@ __device__ __forceinline__ void clock_tick(const ClockArgs& a) {
   const double dT = a.T_amp * sin(2 * PI * a.T_freq * t + a.T_phase);
   c->dT = dT;
   // Eq. 40: a rest length l (1 + alpha_mean dT) <= 0 on any bond is a fault
-  if (!(1.0 + fmin(a.alpha_lo * dT, a.alpha_hi * dT) > 0.0)) c->fault = 1;
+  if (!(1.0 + fmin(a.alpha_lo * dT, a.alpha_hi * dT) > 0.0) && (unsigned long long)n < c->fault)
+    c->fault = (unsigned long long)n;
   c->step = n;
   c->next = n + 1;
   if (a.collide) {
@@ -1456,8 +1457,10 @@ __global__ void __launch_bounds__(256) k_contact(Dev<R> d, const unsigned* gbox,
       const R pen = ra + rb - dist;
       if (!(pen > R(0))) continue;
       V3<R> n;
+      // coincident centres: +z for the voxel with the lower external
+      // id (x-fastest order = lexicographic (k, j, i)), -z for the other
       if (dist > R(0)) n = (R(1) / dist) * dd;
-      else n = mk(R(0), R(0), s < u ? R(1) : R(-1));
+      else n = mk(R(0), R(0), (a.z != b.z ? a.z < b.z : a.y != b.y ? a.y < b.y : a.x < b.x) ? R(1) : R(-1));
       const R4 mob = ss[2 * u + 1];
       const V3<R> Va = ma.inv_m * mk(moa.x, moa.y, moa.z);
       const V3<R> Vb = mb.inv_m * mk(mob.x, mob.y, mob.z);

@@ -5,10 +5,21 @@ import numpy as np
 import pytest
 
 import workloads as W
+from parity import assert_parity, errors, oracle_for
 from paper_1212_2845_b200 import VoxError, from_scene
 from paper_1212_2845_b200.batch import pack
 
 pytestmark = pytest.mark.gpu
+
+
+def _vs_oracle(b, s, sc, st, steps, prec):
+    """Scene s of the batch against its own fp64 oracle run (each
+    packed design is one independent physical evaluation)."""
+    o = oracle_for(sc)
+    o.step(steps)
+    init = sc.initial_state()
+    e = errors(b.state_of(s, st), o.read_state(), init[0], sc.lattice_dim, prec, init=init)
+    assert_parity(e, prec, (sc.name, s))
 
 
 def _cube_variants(K, n=6):
@@ -43,6 +54,7 @@ def test_batch_equals_each_scene_alone(engine, prec, z_stack):
         scale = np.abs(u_ref).max()
         assert np.abs(u - u_ref).max() <= (1e-12 if prec == 64 else 1e-5) * scale, s
         assert np.array_equal(st.latch[b.ext_of[s]], ref.latch)
+        _vs_oracle(b, s, sc, st, 120, prec)
 
 
 @pytest.mark.parametrize("z_stack", [1, "auto"])
@@ -65,6 +77,7 @@ def test_batch_self_collision_stays_inside_each_scene(z_stack):
         lat.step(300)
         u_ref = lat.read_state().pos - sc.initial_state()[0]
         assert np.abs(b.displacement_of(s, st) - u_ref).max() <= 1e-12 * np.abs(u_ref).max()
+        _vs_oracle(b, s, sc, st, 300, 64)
 
 
 def test_batch_rejects_filled_separator():
@@ -98,6 +111,7 @@ def test_batch_y_stacked_cantilevers_equal_alone(prec):
         u_ref = lat.read_state().pos - sc.initial_state()[0]
         u = b.displacement_of(s, st)
         assert np.abs(u - u_ref).max() <= (1e-12 if prec == 64 else 1e-5) * np.abs(u_ref).max(), s
+        _vs_oracle(b, s, sc, st, 400, prec)
 
 
 def test_batch_rejects_filled_separator_row():

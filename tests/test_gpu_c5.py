@@ -41,11 +41,20 @@ def _samples(rng):
     return sorted(pts)
 
 
+def _oracle_dt():
+    """The oracle's own dt for the C5 recipe: Eq. 31-32 over a 32^3 block of it,
+    which holds every material pair of the full grid (tests/test_gpu_full_path)."""
+    s = W.block(32, 32, 32, precision=64)
+    return OracleSim(s.cells, s.lattice_dim, s.materials, s.env, s.origin).dt
+
+
 @pytest.mark.parametrize("engine", ["fused", "two_pass"])
 def test_c5_full_size_sampled_one_step(engine):
     sc = W.block(precision=32)
     lat = from_scene(sc, precision=32, init_state=False, engine=engine)
     assert lat.num_voxels == NX * NY * NZ
+    dt = _oracle_dt()
+    assert lat.dt == dt
     lat.step(3)        # bench warm-up
     lat.step(20)       # graph chunks
     n = lat.steps_done
@@ -80,7 +89,7 @@ def test_c5_full_size_sampled_one_step(engine):
         o = OracleSim(sub, sc.lattice_dim, sc.materials, sc.env,
                       origin=((i - 1) * sc.lattice_dim, (j - 1) * sc.lattice_dim,
                               (k - 1) * sc.lattice_dim))
-        o.set_dt(lat.dt)
+        o.set_dt(dt)        # a 3x3x3 neighbourhood lacks most pairs: C5's (= the oracle's) dt
         o.set_step(n)
         o.set_state(before.pos[q], before.quat[q], before.linmom[q], before.angmom[q],
                     before.latch[q])

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from parity import errors, oracle_for
+from parity import assert_parity, errors, oracle_for
 from paper_1212_2845_b200 import from_scene
 
 pytestmark = pytest.mark.gpu
@@ -52,9 +52,8 @@ def test_fused_matches_oracle(name, prec):
     lat.step(steps - steps // 2)
     o.step(steps)
     g, r = lat.read_state(), o.read_state()
-    e = errors(g, r, sc.initial_state()[0], sc.lattice_dim)
-    assert e["eD"] <= TOL[prec], (name, prec, e)
-    assert np.array_equal(g.latch, r.latch)
+    e = errors(g, r, sc.initial_state()[0], sc.lattice_dim, prec, init=sc.initial_state())
+    assert_parity(e, prec, name)
 
 
 @pytest.mark.parametrize("prec", [32, 64])
@@ -77,10 +76,16 @@ def test_fused_slabs_bitwise(prec):
     ref = from_scene(sc, precision=prec, engine="fused")
     ref.step(77)
     r = _flat(ref.read_state())
+    o = oracle_for(sc)
+    o.step(77)
+    orc = o.read_state()
     for P in (2, 3, 5, 8):
         lat = from_scene(sc, precision=prec, nranks=P, engine="fused")
         lat.step(77)
         assert np.array_equal(_flat(lat.read_state()), r), P
+        init = sc.initial_state()
+        assert_parity(errors(lat.read_state(), orc, init[0], sc.lattice_dim, prec, init=init),
+                      prec, P)
 
 
 def test_fused_engine_switch_and_checkpoint():
@@ -119,5 +124,5 @@ def test_fused_tall_z_chunks_match_oracle(prec):
     lat.step(100)
     o.step(100)
     g, r = lat.read_state(), o.read_state()
-    e = errors(g, r, sc.initial_state()[0], sc.lattice_dim)
-    assert e["eD"] <= {64: 1e-9, 32: 1e-4}[prec], e
+    e = errors(g, r, sc.initial_state()[0], sc.lattice_dim, prec, init=sc.initial_state())
+    assert_parity(e, prec, "tall")

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from parity import errors, run_pair
+from parity import assert_parity, errors, oracle_for, run_pair
 
 pytestmark = pytest.mark.gpu
 SEEDS = range(int(os.environ.get("VX_FUZZ_SEEDS", "30")))   # more for an extended run
@@ -46,17 +46,18 @@ def _scene(seed):
 def test_fuzz_fp64(seed, engine):
     sc = _scene(seed)
     g, o, p0, lat, orc = run_pair(sc, 150, 64, chunks=3, engine=engine)
-    e = errors(g, o, p0, sc.lattice_dim)
-    assert e["eD"] <= 1e-9, (seed, engine, e, sc.cells.shape)
-    assert np.array_equal(g.latch, o.latch)
+    e = errors(g, o, p0, sc.lattice_dim, 64, init=sc.initial_state())
+    assert_parity(e, 64, (seed, engine, sc.cells.shape))
 
 
 @pytest.mark.parametrize("seed", SEEDS)
 def test_fuzz_fp32_fused(seed):
     sc = _scene(seed)
     g, o, p0, lat, orc = run_pair(sc, 150, 32, engine="fused")
-    e = errors(g, o, p0, sc.lattice_dim)
+    e = errors(g, o, p0, sc.lattice_dim, 32, init=sc.initial_state())
     assert e["eD"] <= 1e-4, (seed, e, sc.cells.shape)
+    if e["latch_flips"] == 0:   # a friction threshold decided differently in fp32 moves P
+        assert_parity(e, 32, (seed, sc.cells.shape))
 
 
 @pytest.mark.parametrize("seed", SEEDS)
@@ -67,6 +68,9 @@ def test_fuzz_slabs_and_geometry_bitwise(seed):
     sc = _scene(seed)
     nx = sc.cells.shape[2]
     rng = np.random.default_rng(seed)
+    o = oracle_for(sc)
+    o.step(90)
+    orc = o.read_state()
     for engine in ("fused", "two_pass"):
         ref = from_scene(sc, precision=32, engine=engine)
         ref.step(90)
@@ -78,3 +82,5 @@ def test_fuzz_slabs_and_geometry_bitwise(seed):
         g = lat.read_state()
         for a, b in ((g.pos, r.pos), (g.quat, r.quat), (g.linmom, r.linmom), (g.angmom, r.angmom)):
             assert np.array_equal(a, b), (seed, engine, P)
+        e = errors(g, orc, sc.initial_state()[0], sc.lattice_dim, 32, init=sc.initial_state())
+        assert e["eD"] <= 1e-4, (seed, engine, P, e)     # the slab run against the oracle

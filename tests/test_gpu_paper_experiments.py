@@ -100,7 +100,7 @@ def test_clapper_scheme_equivalence(prec):
     from parity import errors, run_pair
     sc = W.clapper()
     g, o, p0, lat, orc = run_pair(sc, sc.steps, prec, chunks=6)
-    e = errors(g, o, p0, sc.lattice_dim)
+    e = errors(g, o, p0, sc.lattice_dim, prec, init=sc.initial_state())
     assert e["eD"] <= {64: 1e-9, 32: 1e-4}[prec], e
     ijk = sc.voxel_coords()
     tip_a = (ijk[:, 0] == 13) & (ijk[:, 2] == 1)

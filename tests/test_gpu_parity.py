@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from parity import errors, oracle_for, run_pair
+from parity import assert_parity, errors, oracle_for, run_pair
 from paper_1212_2845_b200 import DivergedError, from_scene
 
 pytestmark = pytest.mark.gpu
@@ -20,9 +20,8 @@ TOL = {64: 1e-9, 32: 1e-4}
 
 def _check(scene, steps, prec, chunks=1):
     g, o, p0, lat, orc = run_pair(scene, steps, prec, chunks)
-    e = errors(g, o, p0, scene.lattice_dim)
-    assert e["eD"] <= TOL[prec], (scene.name, prec, e)
-    assert np.array_equal(g.latch, o.latch), (scene.name, prec)
+    e = errors(g, o, p0, scene.lattice_dim, prec, init=scene.initial_state())
+    assert_parity(e, prec, scene.name)
     return g, o, e
 
 
@@ -97,7 +96,7 @@ def test_app_a_regions(prec):
     sc = W.app_a_beam()
     n = 140 if prec == 64 else 50     # fp32 vs fp64 decorrelate on the way to blow-up
     g, o, p0, lat, orc = run_pair(sc, n, prec, chunks=2)
-    e = errors(g, o, p0, sc.lattice_dim)
+    e = errors(g, o, p0, sc.lattice_dim, prec, init=sc.initial_state())
     assert e["eD"] <= TOL[prec], e
     with pytest.raises(FloatingPointError) as eo:
         orc.step(400 - n)

@@ -5,10 +5,25 @@ import numpy as np
 import pytest
 
 import workloads as W
+from parity import assert_parity, errors, oracle_for
 from paper_1212_2845_b200 import from_scene
 from paper_1212_2845_b200 import slab_planes as slab
 
 pytestmark = pytest.mark.gpu
+
+
+def _oracle(sc, steps):
+    o = oracle_for(sc)
+    o.step(steps)
+    return o.read_state()
+
+
+def _vs_oracle(lat, sc, ref, prec, what):
+    """A slab-split run against the fp64 oracle itself (not only against the
+    single-domain GPU run)."""
+    init = sc.initial_state()
+    e = errors(lat.read_state(), ref, init[0], sc.lattice_dim, prec, init=init)
+    assert_parity(e, prec, what)
 
 
 def _flat(st):
@@ -38,6 +53,7 @@ def test_slabs_bitwise_equal_single_domain(name, prec, engine):
     ref.step(150)
     r = _flat(ref.read_state())
     nx = sc.cells.shape[2]
+    orc = _oracle(sc, 150)
     for P in sorted(p for p in {2, 3, 4, 5, 7, 8} if p <= nx):
         lat = from_scene(sc, precision=prec, nranks=P, engine=engine)
         if engine == "two_pass":
@@ -47,6 +63,7 @@ def test_slabs_bitwise_equal_single_domain(name, prec, engine):
             assert lat.launches_per_step == 1 + sum(2 if x >= 3 else 1 for x in w)
         lat.step(150)
         assert np.array_equal(_flat(lat.read_state()), r), (name, prec, P)
+        _vs_oracle(lat, sc, orc, prec, (name, P))
         lat.destroy()
 
 
@@ -95,6 +112,7 @@ def test_slabs_self_collision_bitwise(name, prec, engine):
     pairs = ref.contact_pairs()
     assert ref.num_rebuilds >= 2 and len(pairs) > 0
     nx = sc.cells.shape[2]
+    orc = _oracle(sc, steps)
     for P in (2, 3, 4, 5):
         if P > nx:
             continue
@@ -104,6 +122,7 @@ def test_slabs_self_collision_bitwise(name, prec, engine):
         assert np.array_equal(lat.contact_pairs(), pairs), (name, P)
         assert lat.num_contact_pairs == ref.num_contact_pairs
         assert np.array_equal(_flat(lat.read_state()), r), (name, prec, P)
+        _vs_oracle(lat, sc, orc, prec, (name, P))
         lat.destroy()
 
 

@@ -219,6 +219,35 @@ def app_a_beam():
     return s
 
 
+def strained(scene, seed=1, u=1e-2, rot=1e-2, v=0.05, w=50.0, lift=True):
+    """A seeded, strained initial state for ``scene`` (parity cases that load
+    every term of Eq. 13-24 and 33-35 from the first step): rest sites plus
+    displacements ~ N(0, (u l)^2) per component, orientations near identity
+    (unit quaternion (1, r) / |(1, r)|, r ~ N(0, (rot/2)^2)), velocities ~
+    N(0, v^2) m/s and angular velocities ~ N(0, w^2) rad/s turned into momenta
+    with each voxel's m = rho l^3 and I = m l^2 / 6.  Voxels in the
+    bottom layer are lifted by |u_z| (``lift``) so none starts inside the floor;
+    with ``lift=False`` about half of them start penetrating it.
+    Input generation only: no step of the method is evaluated here."""
+    rng = np.random.Generator(np.random.PCG64([SEED, seed]))
+    pos, quat, P, phi, latch = scene.initial_state()
+    n = len(pos)
+    l = scene.lattice_dim
+    du = rng.normal(size=(n, 3)) * u * l
+    k = scene.voxel_coords()[:, 2]
+    if lift:
+        du[k == 0, 2] = np.abs(du[k == 0, 2])
+    pos = pos + du
+    r = rng.normal(size=(n, 3)) * rot / 2
+    q = np.concatenate([np.ones((n, 1)), r], 1)
+    quat = q / np.linalg.norm(q, axis=1, keepdims=True)
+    mats = scene.cells.ravel()[np.flatnonzero(scene.cells.ravel())]
+    m = np.array([mm["rho"] for mm in scene.materials])[mats - 1] * l ** 3
+    P = P + m[:, None] * rng.normal(size=(n, 3)) * v
+    phi = (m * l * l / 6)[:, None] * rng.normal(size=(n, 3)) * w
+    return pos, quat, P, phi, latch
+
+
 CONFIGS = {
     "C1": cantilever,
     "C2": cube,
