@@ -278,7 +278,10 @@ Vec3 contact_force(const orc_sim* s, int a, int b, double dT) {
   double q = ra + rb - dist;
   if (!(q > 0)) return Vec3();
   Vec3 n;
-  if (dist > 0) n = (1.0 / dist) * d;
+  /* coincident centres (reading R16: closer than 1e-6 l, where the
+   * centre line is rounding noise in any stored representation): +z for the
+   * lower id, -z for the other */
+  if (dist > 1e-6 * s->l) n = (1.0 / dist) * d;
   else n = v3(0, 0, a < b ? 1.0 : -1.0);
   Vec3 Va = (1.0 / ma.m) * s->st[a].P, Vb = (1.0 / mb.m) * s->st[b].P;
   double vnrm = dot(Va - Vb, n);

@@ -1457,9 +1457,10 @@ __global__ void __launch_bounds__(256) k_contact(Dev<R> d, const unsigned* gbox,
       const R pen = ra + rb - dist;
       if (!(pen > R(0))) continue;
       V3<R> n;
-      // coincident centres: +z for the voxel with the lower external
-      // id (x-fastest order = lexicographic (k, j, i)), -z for the other
-      if (dist > R(0)) n = (R(1) / dist) * dd;
+      // coincident centres (reading R16: closer than 1e-6 l): +z for the
+      // voxel with the lower external id (x-fastest order = lexicographic
+      // (k, j, i)), -z for the other
+      if (dist > R(1e-6) * d.l) n = (R(1) / dist) * dd;
       else n = mk(R(0), R(0), (a.z != b.z ? a.z < b.z : a.y != b.y ? a.y < b.y : a.x < b.x) ? R(1) : R(-1));
       const R4 mob = ss[2 * u + 1];
       const V3<R> Va = ma.inv_m * mk(moa.x, moa.y, moa.z);

@@ -97,11 +97,13 @@ def test_clapper_scheme_equivalence(prec):
     each other.  The GPU runs the horizon scheme (surface voxels, hashed grid,
     rebuild on the motion budget); the oracle runs all pairs every
     step (A22).  Same contacts, same state."""
-    from parity import errors, run_pair
+    from parity import assert_parity, errors, run_pair
     sc = W.clapper()
     g, o, p0, lat, orc = run_pair(sc, sc.steps, prec, chunks=6)
     e = errors(g, o, p0, sc.lattice_dim, prec, init=sc.initial_state())
-    assert e["eD"] <= {64: 1e-9, 32: 1e-4}[prec], e
+    # 3000 contact-driven steps: positions at the 100-step bar; momenta, which
+    # carry the stiff contact impulses, within 1e-3 (fp32; measured 4.7e-4)
+    assert_parity(e, prec, "clapper", qpphi_tol={64: 1e-8, 32: 1e-3}[prec])
     ijk = sc.voxel_coords()
     tip_a = (ijk[:, 0] == 13) & (ijk[:, 2] == 1)
     tip_b = (ijk[:, 0] == 13) & (ijk[:, 2] == 5)

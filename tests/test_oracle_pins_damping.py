@@ -263,6 +263,24 @@ def test_contact_two_materials_with_normal_damping():
     assert np.abs(st.linmom[:, 1:]).max() == 0.0
 
 
+@pytest.mark.parametrize("sep,along_z", [(0.0, True), (0.5e-6, True), (2e-6, False)])
+def test_contact_near_coincident_threshold(sep, along_z):
+    """Reading R16: centres closer than 1e-6 l count as coincident (+-z);
+    beyond that the centre line is used."""
+    cells = np.zeros((1, 1, 6), np.uint8)
+    cells[0, 0, 0] = 1
+    cells[0, 0, 5] = 1
+    o, s = sim(cells, [mat()], self_collision=1, zeta_col=0.0)
+    pos, quat, P, phi, latch = s.initial_state()
+    pos[1] = pos[0] + np.array([0.0, sep * L, 0.0])
+    o.set_state(pos, quat, P, phi, latch)
+    o.step(1)
+    st = o.read_state()
+    f = 1e6 * L * (L - sep * L)
+    want = [0, 0, o.dt * f] if along_z else [0, -o.dt * f, 0]
+    assert st.linmom[0] == pytest.approx(want, rel=1e-9, abs=1e-30)
+
+
 def test_contact_coincident_centres_push_along_z():
     """Coincident centres: the normal falls back to +z for the lower
     id, -z for the other; the penalty is k_c (r_a + r_b)."""
