@@ -10,7 +10,11 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvoxsim.so")
+# VX_LIB=checked loads the checked build (device bounds checks and shared-memory
+# race tags; paper_1212_2845_b200/build.py) -- for test runs, never the product path
+LIB_PATH = os.path.join(HERE, {"checked": "libvoxsim_checked.so",
+                               "oldparity": "libvoxsim_oldparity.so"}.get(os.environ.get("VX_LIB", ""),
+                                                                       "libvoxsim.so"))
 
 # status codes (vx_status)
 VX_OK = 0

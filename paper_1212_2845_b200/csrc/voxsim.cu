@@ -172,7 +172,6 @@ struct vx_lattice {
   bool engine_resolved = false;
   bool fused_smem_set[2] = {false, false};
   bool fused_yz_smem_set[2] = {false, false};
-  bool tma_ok = false;                    // TMA-staged fused variant (VX_FUSED_TMA=1; measured slower)
   bool yz_ok = true;                      // (y, z)-mapped fused pass for nz < 64 (VX_FUSED_YZ)
   int fused_ty = 8;                       // rows per fused block (VX_FUSED_TY overrides)
   int fused_waves = 4;                    // block waves per fused launch (VX_FUSED_WAVES)
@@ -739,14 +738,11 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
   // chunks, each recomputing its lowest -z bond)
   const int threads = std::min(256, ((h->nz + 31) / 32) * 32);
   a.zchunks = (h->nz + threads - 1) / threads;
-  // TMA-staged rows need 16-byte aligned rows of every array (nz even); the
-  // rows per block are the most that keep two blocks per SM in shared memory.
-  const bool tma = h->tma_ok && (h->nz % 2 == 0) && a.zchunks == 1;
   // rows per block and planes per segment: forced (tuning, boundary planes),
   // tuned for this range, or the defaults
   const auto tuned = h->geo_tuned.find(fused_key(s, x_begin, x_end));
   const bool have = tuned != h->geo_tuned.end() && tuned->second.first > 0;
-  if (h->yz_ok && !tma && h->nz < 64 && h->ny >= 2) {
+  if (h->yz_ok && h->nz < 64 && h->ny >= 2) {
     // shallow lattice: G rows side by side (vx_fused_yz.cuh); "TY" counts steps of G rows
     const int G = std::min(h->ny, 256 / h->nz);
     const int nthr = ((G * h->nz + 31) / 32) * 32;
@@ -783,8 +779,6 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
     return VX_OK;
   }
   int ty = std::min(ty_force > 0 ? ty_force : (have ? tuned->second.first : h->fused_ty), h->ny);
-  if (tma)
-    while (ty > 1 && fused_tma_smem<R>(ty, threads) > 110 * 1024) --ty;
   a.ty = ty;
   a.ntiles_y = (h->ny + a.ty - 1) / a.ty;
   const int planes = a.p1 - a.p0;
@@ -801,13 +795,6 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
     VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    VX_CUDA(cudaFuncSetAttribute(k_step_fused_tma<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    VX_CUDA(cudaFuncSetAttribute(k_step_fused_tma<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    if (const char* e = std::getenv("VX_CARVEOUT")) {   // experiment: smem carveout percent
-      const int pct = std::atoi(e);
-      VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-      VX_CUDA(cudaFuncSetAttribute(k_step_fused<R, false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    }
     h->fused_smem_set[pi] = true;
   }
   a.nblk0 = a.ntiles_y * segs * a.zchunks;
@@ -819,19 +806,13 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
     segs2 = (a.p1b - a.p0b + a.sx - 1) / a.sx;
   }
   const unsigned grid = (unsigned)(a.ntiles_y * (segs + segs2) * a.zchunks);
-  if (tma) {
-    const size_t smem = fused_tma_smem<R>(a.ty, threads);
-    if (col) k_step_fused_tma<R, true><<<grid, threads, smem, st>>>(d, a);
-    else k_step_fused_tma<R, false><<<grid, threads, smem, st>>>(d, a);
+  const size_t smem = fused_smem<R>(a.ty, threads);
+  if (a.zchunks > 1) {
+    if (col) k_step_fused<R, true, true><<<grid, threads, smem, st>>>(d, a);
+    else k_step_fused<R, false, true><<<grid, threads, smem, st>>>(d, a);
   } else {
-    const size_t smem = fused_smem<R>(a.ty, threads);
-    if (a.zchunks > 1) {
-      if (col) k_step_fused<R, true, true><<<grid, threads, smem, st>>>(d, a);
-      else k_step_fused<R, false, true><<<grid, threads, smem, st>>>(d, a);
-    } else {
-      if (col) k_step_fused<R, true, false><<<grid, threads, smem, st>>>(d, a);
-      else k_step_fused<R, false, false><<<grid, threads, smem, st>>>(d, a);
-    }
+    if (col) k_step_fused<R, true, false><<<grid, threads, smem, st>>>(d, a);
+    else k_step_fused<R, false, false><<<grid, threads, smem, st>>>(d, a);
   }
   return VX_OK;
 }
@@ -1352,7 +1333,6 @@ vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
   // single GPU exercises the multi-rank code: communicator, comm-stream overlap,
   // NCCL inside CUDA graphs
   if (desc->nranks == 1 && desc->nccl_id && std::getenv("VX_FORCE_NCCL")) h->force_nccl = true;
-  if (const char* e = std::getenv("VX_FUSED_TMA")) h->tma_ok = std::atoi(e) != 0;
   if (const char* e = std::getenv("VX_FUSED_YZ")) h->yz_ok = std::atoi(e) != 0;
   if (const char* e = std::getenv("VX_FUSED_TY")) {
     h->fused_ty = std::max(1, std::min(64, std::atoi(e)));
@@ -1678,6 +1658,22 @@ vx_status vx_step(vx_lattice* h, int64_t n) {
   if (h->prec == 32) VX_TRY(run_steps<float>(h, n));
   else VX_TRY(run_steps<double>(h, n));
   h->steps_done += n;
+#ifdef VX_CHECKED
+  {   // device checks (vx_common.cuh): the first failure, as VX_ERR_STATE
+    unsigned long long chk = 0;
+    VX_CUDA(cudaMemcpyFromSymbol(&chk, vx::g_vx_chk, sizeof chk));
+    if (chk) {
+      static const char* what[] = {"?", "state load index out of range", "-z record race (k_step_fused)",
+                                   "edge row race (k_step_fused)", "material index out of range",
+                                   "-y ring race (k_step_fused_yz)", "-z record race (k_step_fused_yz)",
+                                   "state store outside the launch's planes"};
+      const unsigned code = (unsigned)(chk >> 32);
+      return fail(VX_ERR_STATE, std::string("device check failed: ") + (code < 8 ? what[code] : "?") +
+                                    " (code " + std::to_string(code) + ", kernel source line " +
+                                    std::to_string((unsigned)(chk & 0xffffffffu)) + ")");
+    }
+  }
+#endif
   Clock c;
   VX_CUDA(cudaMemcpy(&c, h->clk.p, sizeof c, cudaMemcpyDeviceToHost));
   unsigned long long err = c.err, fault = c.fault;

@@ -7,6 +7,33 @@
 
 namespace vx {
 
+// ---------------------------------------------------------------- device checks
+// The checked build (-DVX_CHECKED, libvoxsim_checked.so; build.py) bounds-checks
+// every state load and store of the step kernels and tags the shared-memory
+// records handed between threads (k_step_fused's -z record and edge row,
+// k_step_fused_yz's -y ring and -z record) with the row that wrote them, so a
+// consumer that finds another row's tag has caught a write-after-read race; it
+// also delays the consumers of cross-warp handoffs to widen any such window.
+// The first failed check is kept as (code << 32) | source line and vx_step
+// reports it as VX_ERR_STATE.  Codes: 1 state load index, 2 -z record race,
+// 3 edge-row race, 4 material index, 5 -y ring race (yz pass), 6 -z record
+// race (yz pass), 7 state store outside the launch's planes.
+// In normal builds VX_CHK compiles to nothing.
+#ifdef VX_CHECKED
+__device__ unsigned long long g_vx_chk = 0ULL;
+#define VX_CHK(cond, code)                                                                      \
+  do {                                                                                          \
+    if (!(cond))                                                                                \
+      atomicCAS(&::vx::g_vx_chk, 0ULL, ((unsigned long long)(code) << 32) | (unsigned)__LINE__); \
+  } while (0)
+#define VX_CHECKED_ONLY(x) x
+#else
+#define VX_CHK(cond, code) \
+  do {                     \
+  } while (0)
+#define VX_CHECKED_ONLY(x)
+#endif
+
 // ---------------------------------------------------------------- layout
 // Per-voxel state, box-indexed (internal id = ((i - xl0) * ny + j) * nz + k,
 // x slowest so an x-slab and each x-plane is one contiguous range):

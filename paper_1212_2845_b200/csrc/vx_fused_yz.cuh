@@ -18,8 +18,12 @@
 namespace vx {
 
 template <class R> size_t fused_yz_smem(int ty, int nz, int g) {
-  // xrec[ty][nz], yring[3][g * nz], zrec[2][g * nz]
-  return sizeof(Rec6<R>) * ((size_t)ty * nz + 5 * (size_t)g * nz);
+  // xrec[ty][nz], yring[3][g * nz], zrec[2][g * nz] (+ their row tags, checked build)
+  return sizeof(Rec6<R>) * ((size_t)ty * nz + 5 * (size_t)g * nz)
+#ifdef VX_CHECKED
+         + sizeof(int) * 5 * (size_t)g * nz
+#endif
+      ;
 }
 
 template <class R, bool COLLIDE>
@@ -33,6 +37,12 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused_yz(D
   Rec6<R>* zrec = yring + 3 * (size_t)gn;
   const int t = threadIdx.x, r = t / nz, k = t - r * nz;
   const bool lane_ok = t < gn;
+#ifdef VX_CHECKED
+  volatile int* rtag = reinterpret_cast<volatile int*>(zrec + 2 * (size_t)gn);   // [3][gn]
+  volatile int* ztag = rtag + 3 * gn;                                             // [2][gn]
+  for (int q = t; q < 5 * gn; q += blockDim.x) rtag[q] = -1;
+  __syncthreads();
+#endif
 
   int bid = blockIdx.x, p0 = a.p0, p1 = a.p1;
   if (bid >= a.nblk0) { bid -= a.nblk0; p0 = a.p0b; p1 = a.p1b; }
@@ -49,6 +59,9 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused_yz(D
   auto idx = [&](int i, int j) { return (uint32_t)i * sx + (uint32_t)j * (uint32_t)nz + (uint32_t)k; };
   const int steps = (j1 - j0 + G - 1) / G;
   auto slot = [&](int m) { return yring + (size_t)((m + 3) % 3) * gn; };   // ring slot of step m >= -1
+  int pl = 0;   // planes done (row tags: stamp of step m of this plane)
+  auto stamp = [&](int m) { return pl * (steps + 1) + m + 1; };
+  (void)stamp;
 
   // -x slots of plane i0: the +x bonds of plane i0 - 1 (halo, recomputed)
   for (int m = 0; m < steps; ++m) {
@@ -56,8 +69,8 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused_yz(D
     if (!lane_ok || j >= j1) continue;
     Rec6<R> rx{};
     if (i0 > 0) {
-      const VS<R> va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i0 - 1, j));
-      const VS<R> vb = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i0, j));
+      const VS<R> va = ldv(d, idx(i0 - 1, j));
+      const VS<R> vb = ldv(d, idx(i0, j));
       if (meta_of(va.p.w) & nb_bit(1)) {
         const AFrame<R> f = a_frame(d, va);
         V3<R> Fa, Ma, Mb;
@@ -74,9 +87,9 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused_yz(D
     if (lane_ok && r == G - 1) {
       Rec6<R> ry{};
       if (j0 > 0) {
-        const VS<R> vh = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0 - 1));
+        const VS<R> vh = ldv(d, idx(i, j0 - 1));
         if (meta_of(vh.p.w) & nb_bit(3)) {
-          const VS<R> vb = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0));
+          const VS<R> vb = ldv(d, idx(i, j0));
           const AFrame<R> f = a_frame(d, vh);
           V3<R> Fa, Ma, Mb;
           bond_eval<1>(d, f.Ra, vh.q, f.ua, f.Va, f.wa, f.mat, vb, dT, Fa, Ma, Mb);
@@ -84,17 +97,18 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused_yz(D
         }
       }
       slot(-1)[t] = ry;
+      VX_CHECKED_ONLY(__threadfence_block(); rtag[2 * gn + t] = stamp(-1));
     }
     for (int m = 0; m < steps; ++m) {
       const int j = j0 + m * G + r;
       const bool act = lane_ok && j < j1;
       const uint32_t id = act ? idx(i, j) : 0u;
       VS<R> cur{};
-      if (act) cur = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id);
+      if (act) cur = ldv(d, id);
       const uint32_t meta = act ? meta_of(cur.p.w) : 0u;
       VS<R> vy{}, vx{};
-      if (meta & nb_bit(3)) vy = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + (uint32_t)nz);
-      if (meta & nb_bit(1)) vx = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + sx);
+      if (meta & nb_bit(3)) vy = ldv(d, id + (uint32_t)nz);
+      if (meta & nb_bit(1)) vx = ldv(d, id + sx);
       if (act && i + 1 < a.nplanes) {   // the next step's +x rows (first touch: HBM) into L2
         int jj = j + G, ii = i + 1;
         if (jj >= j1) { jj -= j1 - j0; ++ii; }
@@ -109,7 +123,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused_yz(D
       // +z neighbour: the next thread's voxel (same row when k + 1 < nz); the
       // last lane of a warp reads it
       VS<R> vz = vs_shfl_down(cur);
-      if ((t & 31) == 31 && (meta & nb_bit(5))) vz = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + 1);
+      if ((t & 31) == 31 && (meta & nb_bit(5))) vz = ldv(d, id + 1);
       V3<R> FX{}, MX{}, BX{}, FY{}, MY{}, BY{}, FZ{}, MZ{}, BZ{};
       if (meta & M_FILLED) {
         const AFrame<R> f = a_frame(d, cur);
@@ -121,6 +135,8 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused_yz(D
       if (lane_ok) {
         zr[t] = rec6(FZ, BZ);
         slot(m)[t] = rec6(FY, BY);
+        VX_CHECKED_ONLY(__threadfence_block(); ztag[(m & 1) * gn + t] = stamp(m);
+                        rtag[((m + 3) % 3) * gn + t] = stamp(m));
       }
       V3<R> F = mk(R(0), R(0), R(0)), M = F;
       if (act) {
@@ -131,7 +147,15 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused_yz(D
       }
       __syncthreads();
       if (!act) continue;
+      VX_CHK(i >= p0 && i < p1, 7);
       if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
+#ifdef VX_CHECKED
+        if ((t & 31) == 0) __nanosleep(((unsigned)(t * 613 + m * 97 + pl * 31)) % 2000u);
+        if (meta & nb_bit(2))
+          VX_CHK(r > 0 ? rtag[((m + 3) % 3) * gn + t - nz] == stamp(m)
+                       : rtag[((m + 2) % 3) * gn + t + (G - 1) * nz] == stamp(m - 1), 5);
+        if (meta & nb_bit(4)) VX_CHK(ztag[(m & 1) * gn + t - 1] == stamp(m), 6);
+#endif
         if (meta & nb_bit(2)) slot_minus(F, M, r > 0 ? slot(m)[t - nz] : slot(m - 1)[t + (G - 1) * nz]);
         if (meta & nb_bit(3)) slot_plus(F, M, FY, MY);
         if (meta & nb_bit(4)) slot_minus(F, M, zr[t - 1]);
@@ -148,6 +172,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused_yz(D
         st_stream(a.opos + id, cur.p);   // empty cell: meta only
       }
     }
+    ++pl;
   }
   if constexpr (COLLIDE) budget_max(d, vmax);
 }

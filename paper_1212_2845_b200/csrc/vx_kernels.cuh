@@ -192,6 +192,12 @@ __device__ __forceinline__ VS<R> ld_vs(const typename VT<R>::R4* __restrict__ po
   return s;
 }
 
+// A voxel's state by local id (bounds-checked in the checked build).
+template <class R> __device__ __forceinline__ VS<R> ldv(const Dev<R>& d, uint32_t i) {
+  VX_CHK(i < d.nloc, 1);
+  return ld_vs<R>(d.pos, d.quat, d.mom, d.ang, i);
+}
+
 template <int AX, class R>
 __device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
                                           const typename VT<R>::R4& qa, V3<R> ua, V3<R> Va,
@@ -201,6 +207,7 @@ __device__ __forceinline__ void bond_eval(const Dev<R>& d, const Rot<R>& Ra,
   const R4& pb = b.p;
   const R4& qb = b.q;
   const int mat_b = meta_of(pb.w) & M_MAT;
+  VX_CHK(mat_a < d.nmat && mat_b < d.nmat, 4);
   const PairC<R> c = d.pair[mat_a * d.nmat + mat_b];
   const R l = d.l;
 
@@ -269,6 +276,7 @@ __device__ __forceinline__ void bond_eval(const Dev<float>& d, const RotP& Ra, c
   const float4& pb = b.p;
   const float4& qb = b.q;
   const int mat_b = meta_of(pb.w) & M_MAT;
+  VX_CHK(mat_a < d.nmat && mat_b < d.nmat, 4);
   const PairC<float> c = d.pair[mat_a * d.nmat + mat_b];
   const float l = d.l;
 
@@ -372,7 +380,7 @@ template <int AX, class R>
 __device__ __forceinline__ void bond_one(const Dev<R>& d, uint32_t ia, uint32_t ib,
                                          const AFrame<R>& f, const typename VT<R>::R4& qa, R dT) {
   using R4 = typename VT<R>::R4;
-  const VS<R> b = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, ib);
+  const VS<R> b = ldv(d, ib);
   V3<R> Fa, Ma, Mbw;
   bond_eval<AX>(d, f.Ra, qa, f.ua, f.Va, f.wa, f.mat, b, dT, Fa, Ma, Mbw);
   const size_t o = (size_t)AX * d.nloc + ia;
@@ -569,6 +577,8 @@ __device__ __forceinline__ R finish_voxel(const Dev<R>& d, uint32_t id, R zb, co
                                           typename VT<R>::R2* __restrict__ oang,
                                           const uint32_t* __restrict__ ext_of_local) {
   using R4 = typename VT<R>::R4;
+  VX_CHK(id < d.nloc, 7);
+  VX_CHK((int)(meta & M_MAT) < d.nmat, 4);
   const MatC<R> mc = d.mat[meta & M_MAT];
   const R4& p = s.p;
   const R4& mo = s.mo;
@@ -798,6 +808,13 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
   VS<R>* edge = reinterpret_cast<VS<R>*>(zrec + 2 * (size_t)nzb);
   Rec6<R>* yrec = reinterpret_cast<Rec6<R>*>(edge + 2 * (nzb / 32));   // thread-private -y slot
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = nzb >> 5;
+#ifdef VX_CHECKED
+  // row tags of the zrec / edge slots (fused_smem reserves them)
+  volatile int* ztag = reinterpret_cast<volatile int*>(yrec + nzb);
+  volatile int* etag = ztag + 2 * nzb;
+  for (int q = threadIdx.x; q < 2 * nzb + 2 * nwarp; q += nzb) ztag[q] = -1;
+  __syncthreads();
+#endif
 
   // z chunks of blockDim voxels (nz > 256): chunk zc covers k in [kz0, kz0 + nzb)
   const int tk = threadIdx.x;
@@ -828,13 +845,13 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
   // next row's two voxels are loaded before this row's bond is evaluated
   if (act) {
     if (i0 > 0) {
-      VS<R> pa = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i0 - 1, j0));
-      VS<R> pb = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i0, j0));
+      VS<R> pa = ldv(d, idx(i0 - 1, j0));
+      VS<R> pb = ldv(d, idx(i0, j0));
       for (int j = j0; j < j1; ++j) {
         VS<R> na = pa, nb = pb;
         if (j + 1 < j1) {
-          na = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i0 - 1, j + 1));
-          nb = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i0, j + 1));
+          na = ldv(d, idx(i0 - 1, j + 1));
+          nb = ldv(d, idx(i0, j + 1));
         }
         Rec6<R> r{};
         if (meta_of(pa.p.w) & nb_bit(1)) {
@@ -861,9 +878,9 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
     Rec6<R>& ry = yrec[tk];   // -y slot record of the current row: +y bond of the row below
     ry = Rec6<R>{};
     if (act) {
-      va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0));
+      va = ldv(d, idx(i, j0));
       if (j0 > 0) {   // halo row j0 - 1: its +y bond only
-        const VS<R> vh = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0 - 1));
+        const VS<R> vh = ldv(d, idx(i, j0 - 1));
         if (meta_of(vh.p.w) & nb_bit(3)) {
           const AFrame<R> f = a_frame(d, vh);
           V3<R> Fa, Ma, Mb;
@@ -882,9 +899,9 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
       const uint32_t meta = (FULL || act) ? meta_of(cur.p.w) : 0u;
       const uint32_t id = idx(i, j);
       if (FULL || (act && (j + 1 < j1 || (meta & nb_bit(3)))))
-        nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
+        nxt = ldv(d, id + nz);
       VS<R> vx;
-      if (FULL || (meta & nb_bit(1))) vx = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + sx);
+      if (FULL || (meta & nb_bit(1))) vx = ldv(d, id + sx);
       // the +x row VX_PF_DIST rows ahead (first touch: HBM) into L2, continuing into the
       // next plane of the segment at the end of the tile
       if (FULL || act) {
@@ -900,8 +917,13 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
       }
       VS<R> vz = vs_shfl_down(cur);
       if (lane == 31 && (meta & nb_bit(5))) {   // the last lane of the block: the next chunk's
-        if (j > j0 && (!ZC || warp + 1 < nwarp)) vz = edge[(par ^ 1) * nwarp + warp + 1];
-        else vz = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + 1);
+        if (j > j0 && (!ZC || warp + 1 < nwarp)) {
+          VX_CHECKED_ONLY(__nanosleep(((unsigned)(warp * 977 + rc * 131)) % 1500u));
+          vz = edge[(par ^ 1) * nwarp + warp + 1];
+          VX_CHK(etag[(par ^ 1) * nwarp + warp + 1] == rc - 1, 3);
+        } else {
+          vz = ldv(d, id + 1);
+        }
       }
       V3<R> FX{}, MX{}, BX{}, FY{}, MY{}, BY{}, FZ{}, MZ{}, BZ{};
       if (FULL || (meta & M_FILLED)) {
@@ -912,14 +934,20 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
         if (FULL || (meta & nb_bit(3)))
           bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nxt, dT, FY, MY, BY);
       }
-      if (lane == 0 && warp > 0 && (FULL || act) && j + 1 < j1) edge[par * nwarp + warp] = nxt;
+      if (lane == 0 && warp > 0 && (FULL || act) && j + 1 < j1) {
+        edge[par * nwarp + warp] = nxt;
+        VX_CHECKED_ONLY(__threadfence_block(); etag[par * nwarp + warp] = rc);
+      }
       Rec6<R>* zr = zrec + (size_t)par * nzb;
-      if (FULL || act) zr[tk] = rec6(FZ, BZ);
+      if (FULL || act) {
+        zr[tk] = rec6(FZ, BZ);
+        VX_CHECKED_ONLY(__threadfence_block(); ztag[par * nzb + tk] = rc);
+      }
       // the first lane of a later z chunk: its -z bond belongs to the chunk below,
       // recomputed here (halo)
       Rec6<R> zlo{};
       if (ZC && tk == 0 && kz0 > 0 && (meta & nb_bit(4))) {
-        const VS<R> vl = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id - 1);
+        const VS<R> vl = ldv(d, id - 1);
         const AFrame<R> f = a_frame(d, vl);
         V3<R> Fa, Ma, Mb;
         bond_eval<2>(d, f.Ra, vl.q, f.ua, f.Va, f.wa, f.mat, cur, dT, Fa, Ma, Mb);
@@ -936,7 +964,19 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
       ry = rec6(FY, BY);
       __syncthreads();
       if (!FULL && !act) return;
+      VX_CHK(i >= p0 && i < p1, 7);
       if (FULL || (meta & (M_FILLED | M_FIXED)) == M_FILLED) {
+#ifdef VX_CHECKED
+        if ((meta & nb_bit(4)) && tk > 0) {   // widen the window of a lapping writer, then check
+          // (longest after a plane's last row: the next write to this slot after it
+          // is the next plane's first row, with no barrier of its own in between)
+          if (lane == 0) __nanosleep(j == j1 - 1 ? 20000u : ((unsigned)(warp * 613 + rc * 97)) % 2000u);
+          const Rec6<R> zz = zr[tk - 1];
+          __threadfence_block();
+          VX_CHK(ztag[par * nzb + tk - 1] == rc, 2);
+          (void)zz;
+        }
+#endif
         if (meta & nb_bit(4)) slot_minus(F, M, (!ZC || tk > 0) ? zr[tk - 1] : zlo);
         if (meta & nb_bit(5)) slot_plus(F, M, FZ, MZ);
         const R v = finish_voxel<R, COLLIDE>(d, id, kf, cur, meta, F, M, a.opos, a.oquat, a.omom,
@@ -955,8 +995,13 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
     for (int j = j0; j < j1; ++j) {
       const uint32_t m = act ? meta_of(va.p.w) : 0u;
       const bool full = __all_sync(0xffffffffu, (m & (M_FILLED | M_FIXED | kXY)) == (M_FILLED | kXY));
-      if (full) row(std::true_type{}, j, va, vb, rc & 1);
-      else row(std::false_type{}, j, va, vb, rc & 1);
+#ifdef VX_RACE_OLDPARITY   // the round-1 parity (restarts per plane): the probe must catch it
+      const int par = (j - j0) & 1;
+#else
+      const int par = rc & 1;
+#endif
+      if (full) row(std::true_type{}, j, va, vb, par);
+      else row(std::false_type{}, j, va, vb, par);
       ++rc;
       va = vb;
     }
@@ -965,223 +1010,11 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
 }
 
 template <class R> size_t fused_smem(int ty, int nzb) {
-  return sizeof(Rec6<R>) * ((size_t)ty * nzb + 3 * (size_t)nzb) + 2 * (size_t)(nzb / 32) * sizeof(VS<R>);
-}
-
-// ------------------------------------------------------------------ fused step, TMA-staged rows
-// Same sweep, same per-voxel arithmetic and order as k_step_fused; the voxel
-// rows it reads -- (i, j) for the voxel and its +z neighbour, (i, j+1) for +y,
-// (i+1, j) for +x -- are staged in shared memory by bulk copies
-// (cp.async.bulk, completion on one mbarrier per slot) issued by one thread
-// two rows ahead, so the compute warps never wait on HBM/L2 latency.
-// Needs nz even (16-byte aligned rows of every SoA array) and nz <= blockDim.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-
-template <class R> struct RowSlot {   // one staged voxel row (SoA, nzb entries)
-  typename VT<R>::R4* pos;
-  typename VT<R>::R4* quat;
-  typename VT<R>::R4* mom;
-  typename VT<R>::R2* ang;
-  __device__ VS<R> at(int k) const {
-    VS<R> v;
-    v.p = pos[k];
-    v.q = quat[k];
-    v.mo = mom[k];
-    v.an = ang[k];
-    return v;
-  }
-};
-template <class R> __device__ __forceinline__ RowSlot<R> row_slot(unsigned char* base, int nzb) {
-  using R4 = typename VT<R>::R4;
-  RowSlot<R> s;
-  s.pos = reinterpret_cast<R4*>(base);
-  s.quat = s.pos + nzb;
-  s.mom = s.quat + nzb;
-  s.ang = reinterpret_cast<typename VT<R>::R2*>(s.mom + nzb);
-  return s;
-}
-template <class R> __host__ __device__ constexpr size_t row_bytes(int nzb) {
-  return (size_t)nzb * (3 * sizeof(typename VT<R>::R4) + sizeof(typename VT<R>::R2));
-}
-
-constexpr int TMA_NX = 3;   // x-row slots: row j in use, rows j+1, j+2 in flight
-
-template <class R> size_t fused_tma_smem(int ty, int nzb) {
-  return TMA_NX * row_bytes<R>(nzb) + sizeof(Rec6<R>) * ((size_t)ty * nzb + 2 * (size_t)nzb) +
-         8 * TMA_NX + 16;
-}
-
-template <class R, bool COLLIDE>
-__global__ void __launch_bounds__(256, 2) k_step_fused_tma(Dev<R> d, FusedArgs<R> a) {
-  using R4 = typename VT<R>::R4;
-  using R2 = typename VT<R>::R2;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int nzb = blockDim.x;
-  const size_t rb = row_bytes<R>(nzb);
-  unsigned char* rows = smem_raw;                              // TMA_NX x-row slots
-  Rec6<R>* xrec = reinterpret_cast<Rec6<R>*>(rows + TMA_NX * rb);
-  Rec6<R>* zrec = xrec + (size_t)a.ty * nzb;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(zrec + 2 * (size_t)nzb) + 15) & ~uintptr_t(15));
-
-  const int k = threadIdx.x;
-  const bool act = k < (int)d.nz;
-  const R kf = floor_base(d, (uint32_t)k);   // once per thread: k is fixed
-  int bid = blockIdx.x, p0 = a.p0, p1 = a.p1;
-  if (bid >= a.nblk0) { bid -= a.nblk0; p0 = a.p0b; p1 = a.p1b; }
-  const int tile = bid % a.ntiles_y;
-  const int seg = bid / a.ntiles_y;
-  const int j0 = tile * a.ty;
-  const int j1 = min(j0 + a.ty, (int)d.ny);
-  const int i0 = p0 + seg * a.sx;
-  const int i1 = min(i0 + a.sx, p1);
-  const uint32_t sx = d.sx, nz = d.nz;
-  const R dT = (R)d.clk->dT;
-  R vmax = R(0);
-  auto idx = [&](int i, int j) { return (uint32_t)i * sx + (uint32_t)j * nz + (uint32_t)k; };
-
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < TMA_NX; ++b) mbar_init(&bars[b], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  // x-row stream: rows (i+1, j) for every row j of every plane i with i+1 in the
-  // box, issued by thread 0 TMA_NX - 1 rows ahead of use
-  long long x_iss = 0;
-  int xp = i0, xj = j0;
-  const uint32_t bytes = (uint32_t)(nz * (3 * sizeof(R4) + sizeof(R2)));
-  auto pump_x = [&](long long upto) {
-    while (x_iss < upto && xp < i1 && xp + 1 < a.nplanes) {
-      const int slot = (int)(x_iss % TMA_NX);
-      const RowSlot<R> s = row_slot<R>(rows + (size_t)slot * rb, nzb);
-      const uint32_t g = (uint32_t)(xp + 1) * sx + (uint32_t)xj * nz;
-      uint64_t* bar = &bars[slot];
-      mbar_expect_tx(bar, bytes);
-      bulk_g2s(s.pos, d.pos + g, nz * sizeof(R4), bar);
-      bulk_g2s(s.quat, d.quat + g, nz * sizeof(R4), bar);
-      bulk_g2s(s.mom, d.mom + g, nz * sizeof(R4), bar);
-      bulk_g2s(s.ang, d.ang + g, nz * sizeof(R2), bar);
-      ++x_iss;
-      if (++xj >= j1) { xj = j0; ++xp; }
-    }
-  };
-  if (threadIdx.x == 0) pump_x(TMA_NX - 1);
-
-  // -x slots of plane i0: the +x bonds of plane i0 - 1 (halo, recomputed)
-  if (act)
-    for (int j = j0; j < j1; ++j) {
-      Rec6<R> r{};
-      if (i0 > 0) {
-        const uint32_t ia = idx(i0 - 1, j);
-        const VS<R> va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, ia);
-        if (meta_of(va.p.w) & nb_bit(1)) {
-          const VS<R> vb = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, ia + sx);
-          const AFrame<R> f = a_frame(d, va);
-          V3<R> Fa, Ma, Mb;
-          bond_eval<0>(d, f.Ra, va.q, f.ua, f.Va, f.wa, f.mat, vb, dT, Fa, Ma, Mb);
-          r = rec6(Fa, Mb);
-        }
-      }
-      xrec[(size_t)(j - j0) * nzb + k] = r;
-    }
-
-  long long xe = 0;   // x-row element in use
-  for (int i = i0; i < i1; ++i) {
-    const bool hasx = i + 1 < a.nplanes;
-    VS<R> va, vb;
-    Rec6<R> ry{};
-    if (act) {
-      va = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0));
-      if (j0 > 0) {   // halo row j0 - 1: its +y bond only
-        const VS<R> vh = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, idx(i, j0 - 1));
-        if (meta_of(vh.p.w) & nb_bit(3)) {
-          const AFrame<R> f = a_frame(d, vh);
-          V3<R> Fa, Ma, Mb;
-          bond_eval<1>(d, f.Ra, vh.q, f.ua, f.Va, f.wa, f.mat, va, dT, Fa, Ma, Mb);
-          ry = rec6(Fa, Mb);
-        }
-      }
-    }
-    for (int j = j0; j < j1; ++j) {
-      const VS<R>& cur = va;
-      VS<R>& nxt = vb;
-      const uint32_t meta = act ? meta_of(cur.p.w) : 0u;
-      const uint32_t id = idx(i, j);
-      if (threadIdx.x == 0 && hasx) pump_x(xe + TMA_NX);
-      if (act && (j + 1 < j1 || (meta & nb_bit(3))))
-        nxt = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + nz);
-      VS<R> vx, vz;
-      if (meta & nb_bit(5)) vz = ld_vs<R>(d.pos, d.quat, d.mom, d.ang, id + 1);   // L1: this row
-      if (hasx) {
-        mbar_wait(&bars[xe % TMA_NX], (uint32_t)((xe / TMA_NX) & 1));
-        if (meta & nb_bit(1)) vx = row_slot<R>(rows + (size_t)(xe % TMA_NX) * rb, nzb).at(k);
-      }
-      V3<R> FX{}, MX{}, BX{}, FY{}, MY{}, BY{}, FZ{}, MZ{}, BZ{};
-      if (meta & M_FILLED) {
-        const AFrame<R> f = a_frame(d, cur);
-        if (meta & nb_bit(5)) bond_eval<2>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vz, dT, FZ, MZ, BZ);
-        if (meta & nb_bit(1)) bond_eval<0>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, vx, dT, FX, MX, BX);
-        if (meta & nb_bit(3)) bond_eval<1>(d, f.Ra, cur.q, f.ua, f.Va, f.wa, f.mat, nxt, dT, FY, MY, BY);
-      }
-      Rec6<R>* zr = zrec + (size_t)((j - j0) & 1) * nzb;
-      if (act) zr[k] = rec6(FZ, BZ);
-      Rec6<R>& xr = xrec[(size_t)(j - j0) * nzb + k];
-      V3<R> F = mk(R(0), R(0), R(0)), M = F;
-      if (meta & nb_bit(0)) { slot_minus(F, M, xr); }
-      if (meta & nb_bit(1)) slot_plus(F, M, FX, MX);
-      if (meta & nb_bit(2)) { slot_minus(F, M, ry); }
-      if (meta & nb_bit(3)) slot_plus(F, M, FY, MY);
-      if (act && (meta & M_FILLED)) xr = rec6(FX, BX);
-      ry = rec6(FY, BY);
-      __syncthreads();   // z records visible; the x-row slot of row j may be refilled
-      if (hasx) ++xe;
-      if (act) {
-        if ((meta & (M_FILLED | M_FIXED)) == M_FILLED) {
-          if (meta & nb_bit(4)) {
-            const Rec6<R>& z = zr[k - 1];
-            slot_minus(F, M, z);
-          }
-          if (meta & nb_bit(5)) slot_plus(F, M, FZ, MZ);
-          const R v = finish_voxel<R, COLLIDE>(d, id, kf, cur, meta, F, M, a.opos, a.oquat, a.omom,
-                                               a.oang, a.ext_of_local);
-          vmax = fmax(vmax, v);
-        } else if (meta & M_FILLED) {   // fixed: copied through unchanged
-          st_stream(a.opos + id, cur.p);
-          st_stream(a.oquat + id, cur.q);
-          st_stream(a.omom + id, cur.mo);
-          st_stream(a.oang + id, cur.an);
-        } else {
-          st_stream(a.opos + id, cur.p);   // empty cell: meta only
-        }
-      }
-      va = vb;
-    }
-  }
-  if constexpr (COLLIDE) budget_max(d, vmax);
+  return sizeof(Rec6<R>) * ((size_t)ty * nzb + 3 * (size_t)nzb) + 2 * (size_t)(nzb / 32) * sizeof(VS<R>)
+#ifdef VX_CHECKED
+         + sizeof(int) * (2 * (size_t)nzb + 2 * (size_t)(nzb / 32))
+#endif
+      ;
 }
 
 // ------------------------------------------------------------------ K5 broadphase

@@ -19,10 +19,10 @@ def _flat(st):
                            st.angmom.ravel(), st.latch.astype(float)])
 
 
-def _run(sc, prec, steps, ty=None, waves=None, nranks=1, tma=None):
-    old = {k: os.environ.get(k) for k in ("VX_FUSED_TY", "VX_FUSED_WAVES", "VX_FUSED_TMA")}
+def _run(sc, prec, steps, ty=None, waves=None, nranks=1):
+    old = {k: os.environ.get(k) for k in ("VX_FUSED_TY", "VX_FUSED_WAVES")}
     try:
-        for k, v in (("VX_FUSED_TY", ty), ("VX_FUSED_WAVES", waves), ("VX_FUSED_TMA", tma)):
+        for k, v in (("VX_FUSED_TY", ty), ("VX_FUSED_WAVES", waves)):
             if v is None:
                 os.environ.pop(k, None)
             else:
@@ -62,5 +62,3 @@ def test_geometry_bitwise(name, prec):
     for ty, waves in ((1, 4), (3, 1), (8, 64), (2, 16)):
         assert np.array_equal(_run(sc, prec, steps, ty, waves), ref), (name, prec, ty, waves)
     assert np.array_equal(_run(sc, prec, steps, nranks=3), ref), (name, prec, "slabs")
-    # the TMA-staged variant of the sweep (VX_FUSED_TMA=1, rows by cp.async.bulk)
-    assert np.array_equal(_run(sc, prec, steps, tma=1), ref), (name, prec, "tma")
