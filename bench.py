@@ -43,19 +43,24 @@ ALG_BYTES = {
     32: {"bonds": 56 + 108, "integrate": 108 + 56 + 56, "fused": 56 + 56},
     64: {"bonds": 112 + 216, "integrate": 216 + 112 + 112, "fused": 112 + 112},
 }
-# Issue side of the fused kernel, counted by ncu on C5 fp32 at the tuned geometry TY=7, SX=32 (profiles/r09_geometry.md, r11):
-# issue slots per voxel-step (smsp__inst_executed / voxels), FP32 lane-operations
-# (scalar FADD/FMUL/FFMA thread-instructions + 2 x the packed FADD2/FMUL2/FFMA2
-# ones) and FLOP (an FMA lane-op = 2) per voxel-step.
-FUSED_COUNTS = {32: {"warp_inst": 890549478 / 33554432, "fp32_ops": 587.1, "flop": 891.4}}   # ncu r13
+# Issue side of the fused kernel (a secondary roof; the headline roofline is HBM,
+# SURVEY 8(d)): counted by ncu on C5 fp32 at the tuned geometry -- issue slots per
+# voxel-step (smsp__inst_executed / voxels), FP32 lane-operations (scalar
+# FADD/FMUL/FFMA thread-instructions + 2 x the packed FADD2/FMUL2/FFMA2 ones) and
+# FLOP (an FMA lane-op = 2) per voxel-step.  These are constants of the kernel
+# binary measured offline (ncu replays each kernel ~40 times, so it cannot run
+# inside the bench); `source` names the profile, and they go stale with every
+# kernel change until the next profile.
+FUSED_COUNTS = {32: {"warp_inst": 890549478 / 33554432, "fp32_ops": 587.1, "flop": 891.4,
+                     "source": "profiles/r13_full.json (ncu --set full, C5 fp32)"}}
 
 
 def alu_roof(prec, ms, voxels, clocks):
-    """The fused single pass is bound by instruction issue, not by HBM: its
-    algorithmic intensity (855 FLOP / 112 B = 7.6 FLOP/B) sits below the FP32
-    ridge but its 29 warp-instructions per voxel need more issue cycles than
-    112 B need HBM time.  Peak = 4 warp-instructions / clock / SM x 148 SMs x
-    the median SM clock of the timed region."""
+    """Secondary roof of the fused single pass: instruction issue.  Its
+    algorithmic intensity (~890 FLOP / 112 B) sits below the FP32 ridge, but
+    its ~26 warp-instructions per voxel need more issue cycles than 112 B need
+    HBM time.  Peak = 4 warp-instructions / clock / SM x 148 SMs x the median
+    SM clock of the timed region."""
     c = FUSED_COUNTS.get(prec)
     if not c:
         return None
@@ -65,7 +70,7 @@ def alu_roof(prec, ms, voxels, clocks):
     fp_peak = 2 * 128 * 148 * mhz * 1e6 / 1e12                 # TFLOP/s (FMA = 2)
     fp = c["flop"] * voxels / (ms / 1e3) / 1e12
     return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
-            "frac": achieved / peak, "warp_inst_per_voxel": c["warp_inst"],
+            "frac": achieved / peak, "warp_inst_per_voxel": c["warp_inst"], "counts_source": c["source"],
             "fp32": {"achieved": fp, "peak": fp_peak, "unit": "TFLOP/s", "frac": fp / fp_peak,
                      "flop_per_voxel": c["flop"], "lane_ops_per_voxel": c["fp32_ops"]},
             "peak_note": f"4 issue/clk/SM x 148 SMs x {mhz:.0f} MHz; FP32 128 lanes/SM"}
@@ -127,6 +132,26 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.rows)}
+
+
+def state_digest(st, ids=None):
+    """Order- and partition-invariant digest of a state: the sum mod 2^64 of a
+    per-voxel hash of (external id, the bit patterns of its 13 state values and
+    latch).  Ranks holding disjoint voxel sets add their sums, so the digest of
+    the final state must be identical at every GPU count (slab invariance:
+    DESIGN.md §7)."""
+    n = len(st.pos)
+    ids = np.arange(n, dtype=np.uint64) if ids is None else np.asarray(ids, np.uint64)
+    words = np.concatenate([st.pos, st.quat, st.linmom, st.angmom,
+                            st.latch.astype(np.float64)[:, None]], 1).view(np.uint64)
+    with np.errstate(over="ignore"):
+        mult = (np.arange(words.shape[1], dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+                + np.uint64(0xBF58476D1CE4E5B9))
+        h = ids * np.uint64(0x94D049BB133111EB)
+        for c in range(words.shape[1]):
+            x = (words[:, c] ^ h) * mult[c]
+            h = (x ^ (x >> np.uint64(31))) + np.uint64(c + 1)
+        return int(h.sum(dtype=np.uint64))
 
 
 def scene_for(name, precision):
@@ -259,35 +284,48 @@ def run_ours(args):
     lat.step(max(args.warmup, 3))
     barrier()
 
-    # ---- timed region: K steps, state resident in HBM.  Per-kernel CUDA events
-    # are recorded inside the timed region (graphs off; launch overhead hidden by
-    # millisecond kernels) unless the lattice is small, where CUDA graphs carry the
-    # step and the kernel breakdown comes from a separate instrumented pass.
-    live = N >= 2_000_000 if args.timing == "auto" else args.timing == "live"
-    # live: event nodes on every 8th step of the timed region (the kernels'
-    # average launch time, at 1/8 of the event overhead)
-    lat.set_instrumentation(live, stride=8)
+    # ---- timed regions: K steps each, state resident in HBM, CUDA graphs (built
+    # by vx_prepare_steps outside the regions).  `repeats` regions are timed and
+    # the median is the value; then one more region of K steps
+    # carries CUDA-event nodes around every launch of EVERY step for the kernel
+    # breakdown and the roofline (the dominant kernel's average launch time).
+    lat.set_instrumentation(False)
     lat.prepare_steps(args.steps)   # graphs built outside the timed region (nothing runs)
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
-    barrier()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    lat.step(args.steps)
-    ev1.record(stream)
-    barrier()
+    region_ms = []
+    for _ in range(max(1, args.repeats)):
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        lat.step(args.steps)
+        ev1.record(stream)
+        barrier()
+        region_ms.append(vd.max_over_ranks([ev0.elapsed_time(ev1)], dist if world > 1 else None,
+                                           "cuda")[0])
     clocks = sampler.stop()
-    ms = ev0.elapsed_time(ev1)
-    if not live:
-        lat.set_instrumentation(True)
-        lat.step(min(args.steps, 50))
+    ms_max = float(np.median(region_ms))
+    value = N * args.steps / (ms_max / 1e3) * (world if replicas else 1)   # whole job
+    # instrumented region: events on every step
+    lat.set_instrumentation(True, stride=1)
+    lat.prepare_steps(args.steps)
+    barrier()
+    ie0 = torch.cuda.Event(enable_timing=True)
+    ie1 = torch.cuda.Event(enable_timing=True)
+    ie0.record(stream)
+    lat.step(args.steps)
+    ie1.record(stream)
+    barrier()
+    instr_ms = vd.max_over_ranks([ie0.elapsed_time(ie1)], dist if world > 1 else None, "cuda")[0]
     kt = lat.kernel_times()
     n_instr = max(1, round(kt["all"][1] / max(lat.launches_per_step, 1)))   # measured steps
     lat.set_instrumentation(False)
-    ms_max = vd.max_over_ranks([ms], dist if world > 1 else None, "cuda")[0]
-    value = N * args.steps / (ms_max / 1e3) * (world if replicas else 1)   # whole job
+    per_rank = None
+    if world > 1:   # each rank's own kernel breakdown (ms per step), gathered on rank 0
+        mine = [kt[k][0] / n_instr for k in ("bonds", "integrate", "other", "all")]
+        per_rank = vd.gather_rows(mine, dist, "cuda")
 
     # ---- roofline of the dominant kernel (live CUDA-event durations)
     x0, x1 = lat.owned_planes()
@@ -312,25 +350,28 @@ def run_ours(args):
             traffic = None
     names = {"bonds": "k_bonds (K3)", "integrate": "k_integrate (K4)",
              "fused": "k_step_fused (K3+K4 single pass)"}
+    # achieved = algorithmic bytes per launch (112 B / voxel-step fused,
+    # 164 + 220 two-pass, fp32) over the dominant kernel's average launch time
+    # measured by the event nodes on every step of the instrumented region
+    instr_step_ms = instr_ms / args.steps
     roof = {"bound": "hbm", "kernel": names[dom],
             "achieved": gbps[dom], "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": gbps[dom] / peak, "frac_of_spec_8000": gbps[dom] / 8000.0,
             "traffic": traffic,
             "traffic_bytes_per_voxel": traffic / vox_rank if traffic else None,
             "alg_bytes_per_voxel": alg[dom], "avg_launch_ms": avg[dom],
+            "launches_timed": int(kt[slot[dom]][1]),
+            "instrumented_region_ms_per_step": instr_step_ms,
+            "kernel_share_of_step": per_step_ms[dom] / instr_step_ms,
             "kernels": {k: {"ms_per_step": per_step_ms[k], "GBps": gbps[k]} for k in kinds},
             "step_GBps_alg": sum(alg[k] for k in kinds) * N / (ms_max / args.steps / 1e3) / 1e9}
+    # the kernel average comes from the same steps as the region around them
+    assert per_step_ms[dom] <= instr_step_ms * 1.001, (per_step_ms[dom], instr_step_ms)
     if fused:
-        # the binding roof of the single pass is instruction issue (alu_roof)
+        # secondary roof: instruction issue (alu_roof), with the FP32 fraction
         alu = alu_roof(args.precision, per_step_ms[dom], vox_rank, clocks)
         if alu:
-            hbm = {k: roof[k] for k in ("bound", "achieved", "peak", "peak_source", "unit", "frac",
-                                        "frac_of_spec_8000", "traffic", "traffic_bytes_per_voxel",
-                                        "alg_bytes_per_voxel")}
-            roof.update({k: alu[k] for k in ("bound", "achieved", "peak", "unit", "frac")})
-            roof["peak_source"] = alu["peak_note"]
             roof["alu"] = alu
-            roof["hbm"] = hbm
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
@@ -366,6 +407,11 @@ def run_ours(args):
                "h2d_bytes_per_step": bi / K, "d2h_bytes_per_step": bo / K,
                "episode": f"set_state (H2D) + {K} steps + read_state (D2H) per episode; "
                           "bytes per step = episode bytes / K"}
+        # digest of the episode's final state (the same initial state and K at
+        # every GPU count): equal bit for bit for every N when the slab split is
+        # invariant, so a SCALE run doubles as the NCCL slab test
+        e2e["final_state_digest"] = f"{state_digest(hout):016x}"
+        e2e["digest_steps"] = K
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None
@@ -389,15 +435,21 @@ def run_ours(args):
                        **({"packing": f"{-(-args.batch // (bt.z_stack * bt.y_stack))} x-blocks x "
                                       f"{bt.y_stack} y-blocks x {bt.z_stack} z-blocks"}
                           if args.batch > 1 else {}),
-                       "timing": "per-kernel CUDA events in the timed region" if live else
-                                 "CUDA graphs; kernel breakdown from a separate instrumented pass",
+                       "timing": f"median of {len(region_ms)} regions of K steps (CUDA graphs, events "
+                                 "on the library stream, max over ranks); kernel breakdown from one "
+                                 "more region with event nodes on every step",
                        "parallelism": f"replicas{world}" if replicas else f"x-slab{world}",
                        "l2": "no flush: working set (state + bond records) >> 126 MB L2"
                              if N > 1_000_000 else "small lattice, L2-resident"},
             "clocks": clocks, "gpu_launches": lat.launches_per_step * args.steps * world,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "achieved_GBps_alg": roof["step_GBps_alg"],
+            "repeats": {"n": len(region_ms), "region_ms": region_ms,
+                        "median_ms": ms_max, "spread": (max(region_ms) - min(region_ms)) / ms_max},
         }
+        if per_rank is not None:   # ms per step: [bonds, fused/integrate, clock+collision, whole step]
+            line["per_rank_ms_per_step"] = {"columns": ["bonds", "fused_or_integrate", "other", "step"],
+                                            "rows": per_rank}
         print(json.dumps(line), flush=True)
     lat.destroy()
     if world > 1:
@@ -415,8 +467,8 @@ def main():
     ap.add_argument("--precision", type=int, default=32)
     ap.add_argument("--engine", default="auto", choices=["auto", "fused", "two_pass"],
                     help="auto: the fused single pass when nz >= 32 (z lanes of a warp), else K3+K4")
-    ap.add_argument("--timing", default="auto", choices=["auto", "live", "graphs"],
-                    help="per-kernel events inside the timed region (live) or CUDA graphs")
+    ap.add_argument("--repeats", type=int, default=5,
+                    help="timed regions of K steps; the value is their median")
     ap.add_argument("--batch", type=int, default=1,
                     help="pack K copies of the config into one lattice (SURVEY 8f f2)")
     ap.add_argument("--z-stack", default="1",

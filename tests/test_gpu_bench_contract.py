@@ -32,6 +32,10 @@ def test_bench_line_ours():
     assert d["gpu_launches"] > 0
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s"          # SURVEY 8(d)'s roof
+    assert r["kernel_share_of_step"] <= 1.001
+    assert d["repeats"]["n"] == 5 and len(d["repeats"]["region_ms"]) == 5
+    assert len(d["e2e"]["final_state_digest"]) == 16
     assert r["traffic"] is None or isinstance(r["traffic"], float)   # ncu bytes per launch
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     e = d["e2e"]
