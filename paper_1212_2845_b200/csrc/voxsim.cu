@@ -11,6 +11,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -24,6 +25,16 @@
 using namespace vx;
 
 namespace {
+
+// NVTX range over a scope (visible in Nsight Systems / ncu --nvtx): one per C ABI
+// call that does work, per replayed graph chunk of steps, and per one-time
+// phase (engine resolution, launch-geometry tuning, topology build).
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 thread_local std::string g_err;
 
@@ -243,6 +254,7 @@ vx_status exclusive_scan_u32(const uint32_t* in, uint32_t* out, unsigned long lo
 // External ids, static meta of every slab, counts, material-pair table and
 // the surface list, built on the device from the grid (vx_topology.cuh).
 vx_status build_topology(vx_lattice* h) {
+  Nvtx nvtx_("vx build topology (K1)");
   const int nx = h->nx, ny = h->ny, nz = h->nz;
   const unsigned long long nbox = (unsigned long long)h->nbox;
   cudaStream_t st = h->stream;
@@ -639,6 +651,7 @@ vx_status launch_fused(vx_lattice* h, const Slab& s, bool col, int x_begin, int 
 // (explicit rounding, tests/test_gpu_geometry.py), so the state the real step
 // then writes is unchanged.  VX_FUSED_TY / VX_FUSED_WAVES fix the geometry.
 template <class R> vx_status tune_fused(vx_lattice* h) {
+  Nvtx nvtx_("vx tune fused geometry");
   if (!h->fused() || h->fused_tune == 0 || !h->geo_tuned.empty()) return VX_OK;
   const bool split = h->emulated || h->nccl();
   const bool col = h->collide();
@@ -1046,6 +1059,7 @@ vx_status sync_state_copies(vx_lattice* h);
 // packed cantilevers (nz = 20, 1) are faster two-pass (34 vs 39, 9 vs 44 us).
 // Both engines produce the same S_{n+1}, so the choice only changes time.
 template <class R> vx_status resolve_engine(vx_lattice* h) {
+  Nvtx nvtx_("vx resolve engine");
   if (h->engine_req != VX_ENGINE_AUTO || h->engine_resolved) return VX_OK;
   h->engine_resolved = true;
   h->clear_graphs();
@@ -1200,6 +1214,7 @@ template <class R> vx_status run_steps(vx_lattice* h, long long n) {
     const long long g = left >= G ? G : left;
     cudaGraphExec_t ex;
     VX_TRY(get_graph<R>(h, g, h->slabs[0].par, pool, &ex));
+    Nvtx r_(h->fused() ? "vx steps graph (fused)" : "vx steps graph (two-pass)");
     VX_CUDA(cudaGraphLaunch(ex, h->stream));
     if (h->fused() && (g & 1)) h->flip();
     left -= g;
@@ -1303,6 +1318,7 @@ vx_status vx_nccl_unique_id(void* out128) {
 }
 
 vx_status vx_create_lattice(const vx_lattice_desc* desc, vx_lattice** out) {
+  Nvtx nvtx_("vx_create_lattice");
   if (!out) return fail(VX_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (!desc || !desc->cells) return fail(VX_ERR_INVALID_ARG, "desc or desc->cells is NULL");
@@ -1531,6 +1547,7 @@ vx_status vx_add_region(vx_lattice* h, int32_t kind, const double o[3], const do
 
 vx_status vx_set_state(vx_lattice* h, const double* pos, const double* quat, const double* lin,
                        const double* ang, const uint8_t* latch) {
+  Nvtx nvtx_("vx_set_state");
   if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
   VX_TRY(set_device(h));
   const long long N = h->N;
@@ -1586,6 +1603,7 @@ int64_t vx_checkpoint_bytes(const vx_lattice* h) {
 }
 
 vx_status vx_save_checkpoint(vx_lattice* h, void* buf, int64_t bytes) {
+  Nvtx nvtx_("vx_save_checkpoint");
   if (!h || !buf || bytes < vx_checkpoint_bytes(h)) return fail(VX_ERR_INVALID_ARG, "bad checkpoint buffer");
   VX_TRY(set_device(h));
   char* p = static_cast<char*>(buf);
@@ -1602,6 +1620,7 @@ vx_status vx_save_checkpoint(vx_lattice* h, void* buf, int64_t bytes) {
 }
 
 vx_status vx_load_checkpoint(vx_lattice* h, const void* buf, int64_t bytes) {
+  Nvtx nvtx_("vx_load_checkpoint");
   if (!h || !buf || bytes < vx_checkpoint_bytes(h)) return fail(VX_ERR_INVALID_ARG, "bad checkpoint buffer");
   VX_TRY(set_device(h));
   const char* p = static_cast<const char*>(buf);
@@ -1640,6 +1659,7 @@ vx_status vx_set_step(vx_lattice* h, int64_t n) {
 }
 
 vx_status vx_prepare_steps(vx_lattice* h, int64_t n) {
+  Nvtx nvtx_("vx_prepare_steps");
   if (!h || n < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
   if (n == 0) return VX_OK;
   VX_TRY(set_device(h));
@@ -1650,6 +1670,7 @@ vx_status vx_prepare_steps(vx_lattice* h, int64_t n) {
 }
 
 vx_status vx_step(vx_lattice* h, int64_t n) {
+  Nvtx nvtx_("vx_step");
   if (!h || n < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
   if (n == 0) return VX_OK;
   VX_TRY(set_device(h));
@@ -1703,6 +1724,7 @@ vx_status vx_step(vx_lattice* h, int64_t n) {
 
 vx_status vx_read_state(vx_lattice* h, double* pos, double* quat, double* lin, double* ang,
                         uint8_t* latch) {
+  Nvtx nvtx_("vx_read_state");
   if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
   VX_TRY(set_device(h));
   const long long N = h->N;
@@ -1728,6 +1750,7 @@ vx_status vx_read_state(vx_lattice* h, double* pos, double* quat, double* lin, d
 
 vx_status vx_read_voxels(vx_lattice* h, const int64_t* ids, int64_t n, double* pos, double* quat,
                          double* lin, double* ang, uint8_t* latch) {
+  Nvtx nvtx_("vx_read_voxels");
   if (!h || (n > 0 && !ids) || n < 0) return fail(VX_ERR_INVALID_ARG, "bad argument");
   if (n == 0) return VX_OK;
   VX_TRY(set_device(h));

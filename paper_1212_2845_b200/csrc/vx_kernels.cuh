@@ -295,7 +295,7 @@ __device__ __forceinline__ void bond_eval(const Dev<float>& d, const RotP& Ra, c
   const f2_t B1 = f2pk(qb.x, qb.y), B2 = f2pk(qb.z, qb.w);
   const f2_t S1 = f2pk(qb.y, qb.x), S2 = f2pk(qb.w, qb.z);
   const f2_t qxy = fma2(Ra.paz, S1, fma2(bc2(-qa.y), B2, fma2(Ra.pax, S2, mul2(bc2(qa.w), B1))));
-  const f2_t qzw = fma2(Ra.paz, sub2(0ull, S2), fma2(bc2(qa.y), B1, fma2(Ra.pax, S1,
+  const f2_t qzw = fma2(Ra.paz, sub2(zero2(), S2), fma2(bc2(qa.y), B1, fma2(Ra.pax, S1,
                                                                         mul2(bc2(qa.w), B2))));
   const float qx = f2lo(qxy), qy = f2hi(qxy), qz = f2lo(qzw), qw = f2hi(qzw);
   const float kth = (qw < 0.f ? -1.f : 1.f) * rotvec_scale(fabsf(qw), qx, qy, qz);
@@ -516,7 +516,7 @@ __device__ __forceinline__ float integrate_store_f32(const Dev<float>& d, uint32
   const float4& mo = s.mo;
   f2_t Pxy = fma2(bc2(d.dt), f2pk(F.x, F.y), f2pk(mo.x, mo.y));
   const float Pz = fmaf(d.dt, F.z, mo.z);
-  if (zero_lat) Pxy = 0ull;
+  if (zero_lat) Pxy = zero2();
   const f2_t uxy = fma2(bc2(mc.dt_m), Pxy, f2pk(p.x, p.y));
   const float uz = fmaf(mc.dt_m, Pz, p.z);
   const f2_t phxy = fma2(bc2(d.dt), f2pk(M.x, M.y), f2pk(s.an.x, s.an.y));
