@@ -378,6 +378,12 @@ def run_ours(args):
     if not args.no_e2e:
         st0 = (sc.initial_state() if st_init is None else
                (st_init.pos, st_init.quat, st_init.linmom, st_init.angmom, st_init.latch))
+        # x-slab ranks move only their own voxels (vx_set/read_state_owned); one
+        # GPU or replicas use the full-state calls
+        owned = world > 1 and not replicas
+        ids = lat.owned_ids() if owned else None
+        if owned:
+            st0 = tuple(a[ids] for a in st0)
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa
         hin = [pin(a) for a in st0]
         from paper_1212_2845_b200 import State
@@ -391,10 +397,10 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         tw = time.perf_counter()
         e0.record(stream)
-        lat.set_state(*hin)
+        (lat.set_state_owned if owned else lat.set_state)(*hin)
         lat.set_step(0)
         lat.step(K)
-        lat.read_state(hout)
+        (lat.read_state_owned if owned else lat.read_state)(hout)
         e1.record(stream)
         barrier()
         tw = time.perf_counter() - tw
@@ -403,14 +409,21 @@ def run_ours(args):
         ems = max(vd.max_over_ranks([ems, tw * 1e3], dist if world > 1 else None, "cuda"))
         bi = sum(a.nbytes for a in hin)
         bo = sum(a.nbytes for a in (hout.pos, hout.quat, hout.linmom, hout.angmom, hout.latch))
+        bi = vd.max_over_ranks([bi], dist if world > 1 else None, "cuda")[0] if owned else bi
+        bo = vd.max_over_ranks([bo], dist if world > 1 else None, "cuda")[0] if owned else bo
         e2e = {"value": N * K / (ems / 1e3) * (world if replicas else 1), "unit": UNIT,
                "h2d_bytes_per_step": bi / K, "d2h_bytes_per_step": bo / K,
                "episode": f"set_state (H2D) + {K} steps + read_state (D2H) per episode; "
-                          "bytes per step = episode bytes / K"}
+                          "bytes per step = episode bytes / K" +
+                          ("; each rank its own voxels (vx_set/read_state_owned), "
+                           "bytes = the largest rank's" if owned else "")}
         # digest of the episode's final state (the same initial state and K at
         # every GPU count): equal bit for bit for every N when the slab split is
         # invariant, so a SCALE run doubles as the NCCL slab test
-        e2e["final_state_digest"] = f"{state_digest(hout):016x}"
+        dg = state_digest(hout, ids)
+        if owned:
+            dg = vd.sum_over_ranks_u64(dg, dist, "cuda")
+        e2e["final_state_digest"] = f"{dg:016x}"
         e2e["digest_steps"] = K
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)

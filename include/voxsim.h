@@ -29,7 +29,8 @@
 extern "C" {
 #endif
 
-#define VOXSIM_ABI_VERSION 2   /* 2: vx_prepare_steps, vx_set_batch_y/_z, VX_ENGINE_AUTO default */
+#define VOXSIM_ABI_VERSION 3   /* 2: vx_prepare_steps, vx_set_batch_y/_z, VX_ENGINE_AUTO default;
+                                  3: owned-voxel state I/O (vx_num_owned ...) */
 
 typedef struct vx_lattice vx_lattice; /* opaque, library-owned */
 
@@ -187,6 +188,26 @@ vx_status vx_read_state(vx_lattice* h, double* pos, double* quat, double* linmom
  * [0,N) or not owned by this rank when nranks > 1). */
 vx_status vx_read_voxels(vx_lattice* h, const int64_t* ids, int64_t n, double* pos,
                          double* quat, double* linmom, double* angmom, uint8_t* latch);
+
+/* Owned-voxel state I/O (one rank per GPU, nranks > 1): the voxels of this
+ * handle's x-slab (vx_owned_planes), in ascending external id -- each rank
+ * moves only its own share of the state instead of the global arrays.  No
+ * collective; with nranks = 1 (or emulated slabs) the owned voxels are all N.
+ * The state lives in the slab's owned planes; ghost planes are refreshed from
+ * the neighbours by every step's exchange, so setting the owned
+ * voxels on every rank sets the global state.
+ *   vx_num_owned: M (>= 0; -1 on a NULL handle)
+ *   vx_owned_ids: the M external ids into ids[M] (caller-owned)
+ *   vx_set_state_owned / vx_read_state_owned: arrays of M entries in that
+ *     order, layout as vx_set_state / vx_read_state (NULL skips a part; a
+ *     set also forces a collision rebuild).  Errors: INVALID_ARG (NULL handle),
+ *     CUDA. */
+int64_t vx_num_owned(const vx_lattice* h);
+vx_status vx_owned_ids(const vx_lattice* h, int64_t* ids);
+vx_status vx_set_state_owned(vx_lattice* h, const double* pos, const double* quat,
+                             const double* linmom, const double* angmom, const uint8_t* latch);
+vx_status vx_read_state_owned(vx_lattice* h, double* pos, double* quat, double* linmom,
+                              double* angmom, uint8_t* latch);
 
 /* Queries (plain values; 0 / -1 on a NULL handle). */
 double vx_dt(const vx_lattice* h);                 /* stable timestep (s), 0 before set_materials */

@@ -97,12 +97,16 @@ SIGNATURES = {
     "vx_nccl_unique_id": (_I32, [_P]),
     "vx_slab_planes": (_I32, [_I32, _I32, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "vx_abi_version": (_I32, []),
+    "vx_num_owned": (_I64, [_P]),
+    "vx_owned_ids": (_I32, [_P, _P]),
+    "vx_set_state_owned": (_I32, [_P, _P, _P, _P, _P, _P]),
+    "vx_read_state_owned": (_I32, [_P, _P, _P, _P, _P, _P]),
 }
 
 _lib = None
 
 
-ABI_VERSION = 2   # include/voxsim.h VOXSIM_ABI_VERSION
+ABI_VERSION = 3   # include/voxsim.h VOXSIM_ABI_VERSION
 
 
 def load():

@@ -110,6 +110,10 @@ struct Slab {
   DevBuf recA, recB, recC, fextd, cf, meta_d, ext_of_local;
   DevBuf sidx;                            // global surface index per local voxel (collision)
   DevBuf meta_static_d;                  // static meta bits, local box order (K1)
+  // owned-voxel I/O (vx_read_state_owned): local id, global box id and position
+  // in the owned order of this slab's owned voxels
+  DevBuf own_lid, own_gid, own_dst;
+  long long own_n = 0;
   DevBuf& pos() { return buf[par][0]; }
   DevBuf& quat() { return buf[par][1]; }
   DevBuf& mom() { return buf[par][2]; }
@@ -166,6 +170,11 @@ struct vx_lattice {
   double cutoff = 0;
   // staging of the external fp64 state (vx_set_state / vx_read_state), kept between calls
   DevBuf stage_ext, stage_box;
+  // owned-voxel I/O: external ids of the voxels in the owned planes, ascending,
+  // and their global box ids on the device (built on first use)
+  std::vector<int64_t> owned_ext;
+  DevBuf owned_box_d;
+  bool owned_ready = false;
   // graphs
   std::map<long long, cudaGraphExec_t> graphs;
   // instrumentation
@@ -1744,6 +1753,131 @@ vx_status vx_read_state(vx_lattice* h, double* pos, double* quat, double* lin, d
   if (lin) VX_CUDA(cudaMemcpyAsync(lin, e + (size_t)N * 7, (size_t)N * 24, cudaMemcpyDeviceToHost, h->stream));
   if (ang) VX_CUDA(cudaMemcpyAsync(ang, e + (size_t)N * 10, (size_t)N * 24, cudaMemcpyDeviceToHost, h->stream));
   if (latch) VX_CUDA(cudaMemcpyAsync(latch, el, (size_t)N, cudaMemcpyDeviceToHost, h->stream));
+  VX_CUDA(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+// The owned-voxel lists (vx_num_owned ...), built once.
+static vx_status ensure_owned(vx_lattice* h) {
+  if (h->owned_ready) return VX_OK;
+  const long long lo = (long long)h->x0 * h->plane, hi = (long long)h->x1 * h->plane;
+  h->owned_ext.clear();
+  std::vector<long long> box;
+  std::vector<std::vector<long long>> lid(h->slabs.size()), gid(h->slabs.size()), dst(h->slabs.size());
+  for (long long e = 0; e < h->N; ++e) {
+    const long long g = h->box_of_ext[e];
+    if (g < lo || g >= hi) continue;
+    const long long t = (long long)h->owned_ext.size();
+    h->owned_ext.push_back(e);
+    box.push_back(g);
+    const long long x = g / h->plane;
+    for (size_t q = 0; q < h->slabs.size(); ++q) {
+      const Slab& s = h->slabs[q];
+      if (x >= s.x0 && x < s.x1) {
+        lid[q].push_back(g - s.box_base);
+        gid[q].push_back(g);
+        dst[q].push_back(t);
+      }
+    }
+  }
+  const size_t M = box.size();
+  VX_TRY(h->owned_box_d.alloc(M * 8));
+  if (M) VX_CUDA(cudaMemcpy(h->owned_box_d.p, box.data(), M * 8, cudaMemcpyHostToDevice));
+  for (size_t q = 0; q < h->slabs.size(); ++q) {
+    Slab& s = h->slabs[q];
+    const size_t m = lid[q].size();
+    s.own_n = (long long)m;
+    VX_TRY(s.own_lid.alloc(m * 8));
+    VX_TRY(s.own_gid.alloc(m * 8));
+    VX_TRY(s.own_dst.alloc(m * 8));
+    if (!m) continue;
+    VX_CUDA(cudaMemcpy(s.own_lid.p, lid[q].data(), m * 8, cudaMemcpyHostToDevice));
+    VX_CUDA(cudaMemcpy(s.own_gid.p, gid[q].data(), m * 8, cudaMemcpyHostToDevice));
+    VX_CUDA(cudaMemcpy(s.own_dst.p, dst[q].data(), m * 8, cudaMemcpyHostToDevice));
+  }
+  h->owned_ready = true;
+  return VX_OK;
+}
+
+int64_t vx_num_owned(const vx_lattice* h) {
+  if (!h) return -1;
+  if (vx_lattice* m = const_cast<vx_lattice*>(h); ensure_owned(m) != VX_OK) return -1;
+  return (int64_t)h->owned_ext.size();
+}
+
+vx_status vx_owned_ids(const vx_lattice* h, int64_t* ids) {
+  if (!h || !ids) return fail(VX_ERR_INVALID_ARG, "bad argument");
+  VX_TRY(ensure_owned(const_cast<vx_lattice*>(h)));
+  if (!h->owned_ext.empty()) std::memcpy(ids, h->owned_ext.data(), h->owned_ext.size() * 8);
+  return VX_OK;
+}
+
+vx_status vx_set_state_owned(vx_lattice* h, const double* pos, const double* quat, const double* lin,
+                             const double* ang, const uint8_t* latch) {
+  Nvtx nvtx_("vx_set_state_owned");
+  if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
+  VX_TRY(set_device(h));
+  VX_TRY(ensure_owned(h));
+  const long long M = (long long)h->owned_ext.size();
+  if (M == 0) return VX_OK;
+  DevBuf& b = h->stage_ext;
+  const size_t off[5] = {0, (size_t)M * 3, (size_t)M * 7, (size_t)M * 10, (size_t)M * 13};
+  if (b.bytes < (size_t)M * 13 * 8 + (size_t)M) VX_TRY(b.alloc((size_t)M * 13 * 8 + (size_t)M));
+  double* bd = b.as<double>();
+  uint8_t* bl = reinterpret_cast<uint8_t*>(bd + off[4]);
+  if (pos) VX_CUDA(cudaMemcpyAsync(bd + off[0], pos, (size_t)M * 24, cudaMemcpyHostToDevice, h->stream));
+  if (quat) VX_CUDA(cudaMemcpyAsync(bd + off[1], quat, (size_t)M * 32, cudaMemcpyHostToDevice, h->stream));
+  if (lin) VX_CUDA(cudaMemcpyAsync(bd + off[2], lin, (size_t)M * 24, cudaMemcpyHostToDevice, h->stream));
+  if (ang) VX_CUDA(cudaMemcpyAsync(bd + off[3], ang, (size_t)M * 24, cudaMemcpyHostToDevice, h->stream));
+  if (latch) VX_CUDA(cudaMemcpyAsync(bl, latch, (size_t)M, cudaMemcpyHostToDevice, h->stream));
+  const long long* boe = h->owned_box_d.as<long long>();
+  for (const Slab& s : h->slabs) {   // entry e goes to box owned_box[e] (any slab whose box holds it)
+    if (h->prec == 32)
+      k_scatter_state<float><<<grid_of(M), 256, 0, h->stream>>>(
+          make_dev<float>(h, s), boe, M, s.box_base, pos ? bd + off[0] : nullptr, quat ? bd + off[1] : nullptr,
+          lin ? bd + off[2] : nullptr, ang ? bd + off[3] : nullptr, latch ? bl : nullptr, h->origin[0],
+          h->origin[1], h->origin[2]);
+    else
+      k_scatter_state<double><<<grid_of(M), 256, 0, h->stream>>>(
+          make_dev<double>(h, s), boe, M, s.box_base, pos ? bd + off[0] : nullptr, quat ? bd + off[1] : nullptr,
+          lin ? bd + off[2] : nullptr, ang ? bd + off[3] : nullptr, latch ? bl : nullptr, h->origin[0],
+          h->origin[1], h->origin[2]);
+    VX_CUDA(cudaGetLastError());
+  }
+  VX_CUDA(cudaStreamSynchronize(h->stream));
+  h->ss_dirty = true;
+  return set_force_rebuild(h);
+}
+
+vx_status vx_read_state_owned(vx_lattice* h, double* pos, double* quat, double* lin, double* ang,
+                              uint8_t* latch) {
+  Nvtx nvtx_("vx_read_state_owned");
+  if (!h) return fail(VX_ERR_INVALID_ARG, "NULL handle");
+  VX_TRY(set_device(h));
+  VX_TRY(ensure_owned(h));
+  const long long M = (long long)h->owned_ext.size();
+  if (M == 0) return VX_OK;
+  DevBuf& b = h->stage_ext;
+  if (b.bytes < (size_t)M * 13 * 8 + (size_t)M) VX_TRY(b.alloc((size_t)M * 13 * 8 + (size_t)M));
+  double* o = b.as<double>();
+  uint8_t* ol = reinterpret_cast<uint8_t*>(o + (size_t)M * 13);
+  for (const Slab& s : h->slabs) {
+    if (!s.own_n) continue;
+    if (h->prec == 32)
+      k_gather_owned<float><<<grid_of(s.own_n), 256, 0, h->stream>>>(
+          make_dev<float>(h, s), s.own_lid.as<long long>(), s.own_gid.as<long long>(), s.own_dst.as<long long>(),
+          s.own_n, M, o, ol, h->origin[0], h->origin[1], h->origin[2]);
+    else
+      k_gather_owned<double><<<grid_of(s.own_n), 256, 0, h->stream>>>(
+          make_dev<double>(h, s), s.own_lid.as<long long>(), s.own_gid.as<long long>(), s.own_dst.as<long long>(),
+          s.own_n, M, o, ol, h->origin[0], h->origin[1], h->origin[2]);
+    VX_CUDA(cudaGetLastError());
+  }
+  if (pos) VX_CUDA(cudaMemcpyAsync(pos, o, (size_t)M * 24, cudaMemcpyDeviceToHost, h->stream));
+  if (quat) VX_CUDA(cudaMemcpyAsync(quat, o + (size_t)M * 3, (size_t)M * 32, cudaMemcpyDeviceToHost, h->stream));
+  if (lin) VX_CUDA(cudaMemcpyAsync(lin, o + (size_t)M * 7, (size_t)M * 24, cudaMemcpyDeviceToHost, h->stream));
+  if (ang) VX_CUDA(cudaMemcpyAsync(ang, o + (size_t)M * 10, (size_t)M * 24, cudaMemcpyDeviceToHost, h->stream));
+  if (latch) VX_CUDA(cudaMemcpyAsync(latch, ol, (size_t)M, cudaMemcpyDeviceToHost, h->stream));
   VX_CUDA(cudaStreamSynchronize(h->stream));
   return VX_OK;
 }

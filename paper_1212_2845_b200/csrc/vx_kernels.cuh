@@ -1421,6 +1421,35 @@ __global__ void k_read_ids(Dev<R> d, const long long* lids, const long long* gid
   latch[e] = (meta_of(p.w) & M_LATCH) ? 1 : 0;
 }
 
+// Owned-voxel gather (vx_read_state_owned): entries dst[e] of the output
+// arrays from local id lid[e] (global box id gid[e]) of one slab.
+template <class R>
+__global__ void k_gather_owned(Dev<R> d, const long long* lid, const long long* gid, const long long* dst,
+                               long long n, long long m, double* out, uint8_t* latch, double ox, double oy,
+                               double oz) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const long long li = lid[e], g = gid[e], t = dst[e];
+  const long long nyz = (long long)d.ny * d.nz;
+  const long long i = g / nyz, j = (g / d.nz) % d.ny, k = g % d.nz;
+  const double l = d.l_d;
+  const auto p = d.pos[li];
+  const auto q = d.quat[li];
+  const auto mo = d.mom[li];
+  const auto an = d.ang[li];
+  double* pos = out;
+  double* quat = out + m * 3;
+  double* lin = out + m * 7;
+  double* ang = out + m * 10;
+  pos[3 * t] = site(ox, l, i) + (double)p.x;
+  pos[3 * t + 1] = site(oy, l, j) + (double)p.y;
+  pos[3 * t + 2] = site(oz, l, k) + (double)p.z;
+  quat[4 * t] = q.w; quat[4 * t + 1] = q.x; quat[4 * t + 2] = q.y; quat[4 * t + 3] = q.z;
+  lin[3 * t] = mo.x; lin[3 * t + 1] = mo.y; lin[3 * t + 2] = mo.z;
+  ang[3 * t] = an.x; ang[3 * t + 1] = an.y; ang[3 * t + 2] = mo.w;
+  latch[t] = (meta_of(p.w) & M_LATCH) ? 1 : 0;
+}
+
 // Merge static meta bits (material, filled, fixed, surface, ext, neighbours)
 // with the dynamic latch bit.
 template <class R>

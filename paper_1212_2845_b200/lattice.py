@@ -191,6 +191,42 @@ class Lattice:
                                       _ptr(out.angmom), _ptr(out.latch)))
         return out
 
+    # ------------------------------------------------------------ owned-voxel I/O
+    def owned_ids(self):
+        """External ids of the voxels in this rank's slab, ascending (vx_owned_ids)."""
+        m = int(N.load().vx_num_owned(self._h))
+        if m < 0:
+            raise VoxError(m, "vx_num_owned failed")
+        ids = np.empty(m, np.int64)
+        if m:
+            _check(N.load().vx_owned_ids(self._h, ids.ctypes.data))
+        return ids
+
+    def set_state_owned(self, pos=None, quat=None, linmom=None, angmom=None, latch=None):
+        """State of this rank's voxels only, in owned_ids() order (vx_set_state_owned)."""
+        m = int(N.load().vx_num_owned(self._h))
+        arrs = [_arr(a, m, c, t, nm)
+                for a, c, t, nm in ((pos, 3, np.float64, "pos"), (quat, 4, np.float64, "quat"),
+                                    (linmom, 3, np.float64, "linmom"),
+                                    (angmom, 3, np.float64, "angmom"), (latch, 0, np.uint8, "latch"))]
+        _check(N.load().vx_set_state_owned(self._h, *[_ptr(a) for a in arrs]))
+
+    def read_state_owned(self, out: State | None = None) -> State:
+        """State of this rank's voxels, in owned_ids() order (vx_read_state_owned)."""
+        m = int(N.load().vx_num_owned(self._h))
+        if out is None:
+            out = State(np.empty((m, 3)), np.empty((m, 4)), np.empty((m, 3)), np.empty((m, 3)),
+                        np.empty(m, np.uint8))
+        else:
+            for a, c, t, nm in ((out.pos, 3, np.float64, "pos"), (out.quat, 4, np.float64, "quat"),
+                                (out.linmom, 3, np.float64, "linmom"),
+                                (out.angmom, 3, np.float64, "angmom"),
+                                (out.latch, 0, np.uint8, "latch")):
+                _arr(a, m, c, t, nm, out=True)
+        _check(N.load().vx_read_state_owned(self._h, _ptr(out.pos), _ptr(out.quat), _ptr(out.linmom),
+                                            _ptr(out.angmom), _ptr(out.latch)))
+        return out
+
     def read_voxels(self, ids) -> State:
         ids = np.ascontiguousarray(ids, dtype=np.int64)
         n = len(ids)

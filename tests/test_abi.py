@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in _declared() if not hasattr(lib, n)]
     assert not missing, missing
     assert set(_declared()) == set(_native.SIGNATURES)
-    assert lib.vx_abi_version() == 2
+    assert lib.vx_abi_version() == 3
 
 
 def test_no_cpu_fallback_without_device():

@@ -11,6 +11,8 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from conftest import ROOT
+
 
 def _free_port():
     s = socket.socket()
@@ -85,8 +87,12 @@ def _worker(rank, world, port, q):
     vmax = torch.tensor([float(np.abs(state[x0 * plane:x1 * plane, 1]).max())], dtype=torch.float64)
     dist.all_reduce(vmax, op=dist.ReduceOp.MAX)
     out["vmax_ok"] = float(vmax) == float(np.abs(state[:, 1]).max())
-    # 5. max over ranks of per-rank times
+    # 5. max over ranks of per-rank times, the per-rank breakdown rows and the
+    #    wrap-around digest sum bench.py uses (uint64 through int64 all-reduce)
     out["max"] = vd.max_over_ranks([1.0 + rank, 10.0 - rank], dist)
+    out["rows"] = vd.gather_rows([float(rank), 2.0 * rank], dist)
+    big = [0xFFFFFFFFFFFFFFF0 - 7 * r for r in range(world)]
+    out["u64"] = (vd.sum_over_ranks_u64(big[rank], dist), sum(big) & 0xFFFFFFFFFFFFFFFF)
     dist.destroy_process_group()
     q.put((rank, out))
 
@@ -112,3 +118,31 @@ def test_multirank_host_logic_gloo(world):
         assert res[r]["ids_equal"] and res[r]["ghosts_ok"]
         assert res[r]["table_ok"] and res[r]["vmax_ok"]
         assert res[r]["max"] == [float(world), 10.0]
+        assert res[r]["rows"] == [[float(q), 2.0 * q] for q in range(world)]
+        assert res[r]["u64"][0] == res[r]["u64"][1]
+
+
+def test_state_digest_is_partition_invariant():
+    """bench.py's final-state digest: the sum over disjoint owned sets (ranks)
+    equals the digest of the whole state, whatever the split; any changed bit
+    changes it."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    from paper_1212_2845_b200.lattice import State
+    rng = np.random.default_rng(0)
+    n = 1000
+    st = State(rng.normal(size=(n, 3)), rng.normal(size=(n, 4)), rng.normal(size=(n, 3)),
+               rng.normal(size=(n, 3)), (rng.random(n) < 0.3).astype(np.uint8))
+    whole = bench.state_digest(st)
+    for parts in (2, 3, 8):
+        cuts = np.sort(rng.choice(np.arange(1, n), parts - 1, replace=False))
+        tot = 0
+        for ids in np.split(np.arange(n), cuts):
+            sub = State(st.pos[ids], st.quat[ids], st.linmom[ids], st.angmom[ids], st.latch[ids])
+            tot = (tot + bench.state_digest(sub, ids)) & 0xFFFFFFFFFFFFFFFF
+        assert tot == whole
+    st.pos[17, 1] = np.nextafter(st.pos[17, 1], np.inf)
+    assert bench.state_digest(st) != whole
