@@ -779,6 +779,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+
 // Thread k's +z neighbour is thread k+1's own voxel: a warp shuffle of its
 // registers; lane 31 takes it from the next warp's lane 0 through shared
 // memory (written before the previous row's barrier).
