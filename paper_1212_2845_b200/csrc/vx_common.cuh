@@ -264,7 +264,6 @@ struct RotP {
   f2_t c0, c1, c2;          // (m00, m10), (m01, m11), (m02, m12)
   float m20, m21, m22;
   float dd0, dd1, dd2;      // m_ii - 1, formed without cancellation
-  f2_t pax, paz;            // (-x, x), (z, -z): sign pairs of q for q* (x) q_b
 };
 // Same formulas and operation order as rotation(): e.g. m10 = 2 (x y + w z),
 // dd0 = -2 (y^2 + z^2); pairs Q1 = (x, y), Q2 = (z, w) of the quaternion.
@@ -285,8 +284,6 @@ __device__ __forceinline__ RotP rotation_p(float x, float y, float z, float w) {
   r.dd2 = xmul(-2.f, xfma(y, y, xmul(x, x)));
   r.c0 = add2(t0, f2pk(1.f, 0.f));
   r.c1 = add2(t1, f2pk(0.f, 1.f));
-  r.pax = f2pk(-x, x);
-  r.paz = f2pk(z, -z);
   r.m20 = f2lo(r2);
   r.m21 = f2hi(r2);
   r.m22 = xadd(1.f, r.dd2);

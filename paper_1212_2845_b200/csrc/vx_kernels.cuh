@@ -288,15 +288,16 @@ __device__ __forceinline__ void bond_eval(const Dev<float>& d, const RotP& Ra, c
   else t = mk(Ra.m20, Ra.m21, Ra.dd2);
   const V3<float> dv = to_bond<AX>(xfma3(l, t, mulT(Ra, du)));
 
-  // q_rel = q_a* q_b, with the swapped pairs (by, bx), (bw, bz) and the
-  // per-voxel sign pairs (-ax, ax), (az, -az):
-  //   (qx, qy) = aw (bx, by) + (-ax, ax) (bw, bz) - ay (bz, bw) + (az, -az) (by, bx)
-  //   (qz, qw) = aw (bz, bw) + (-ax, ax) (by, bx) + ay (bx, by) - (az, -az) (bw, bz)
+  // q_rel = q_a* q_b as two pair products, q_a's components broadcast (the
+  // scalar operand of FFMA2 / FMUL2) against signed, swapped pairs of q_b:
+  //   (qx, qy) = aw (bx, by) + ax (-bw, bz) - ay (bz, bw) + az (by, -bx)
+  //   (qz, qw) = aw (bz, bw) + ax (-by, bx) + ay (bx, by) + az (-bw, bz)
+  // (per lane the same fma chain as the scalar formula: ax (-bw) = (-ax) bw
+  // exactly; signs on q_a's side made the compiler materialise broadcast pairs)
   const f2_t B1 = f2pk(qb.x, qb.y), B2 = f2pk(qb.z, qb.w);
-  const f2_t S1 = f2pk(qb.y, qb.x), S2 = f2pk(qb.w, qb.z);
-  const f2_t qxy = fma2(Ra.paz, S1, fma2(bc2(-qa.y), B2, fma2(Ra.pax, S2, mul2(bc2(qa.w), B1))));
-  const f2_t qzw = fma2(Ra.paz, sub2(zero2(), S2), fma2(bc2(qa.y), B1, fma2(Ra.pax, S1,
-                                                                        mul2(bc2(qa.w), B2))));
+  const f2_t Wn = f2pk(-qb.w, qb.z), Yn = f2pk(qb.y, -qb.x), Yp = f2pk(-qb.y, qb.x);
+  const f2_t qxy = fma2(bc2(qa.z), Yn, fma2(bc2(-qa.y), B2, fma2(bc2(qa.x), Wn, mul2(bc2(qa.w), B1))));
+  const f2_t qzw = fma2(bc2(qa.z), Wn, fma2(bc2(qa.y), B1, fma2(bc2(qa.x), Yp, mul2(bc2(qa.w), B2))));
   const float qx = f2lo(qxy), qy = f2hi(qxy), qz = f2lo(qzw), qw = f2hi(qzw);
   const float kth = (qw < 0.f ? -1.f : 1.f) * rotvec_scale(fabsf(qw), qx, qy, qz);
   const f2_t thxy = mul2(bc2(kth), qxy);
@@ -993,19 +994,41 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
       }
     };
     constexpr uint32_t kXY = nb_bit(0) | nb_bit(1) | nb_bit(2) | nb_bit(3);
-    for (int j = j0; j < j1; ++j) {
-      const uint32_t m = act ? meta_of(va.p.w) : 0u;
-      const bool full = __all_sync(0xffffffffu, (m & (M_FILLED | M_FIXED | kXY)) == (M_FILLED | kXY));
+    auto is_full = [&](const VS<R>& v) {
+      const uint32_t m = act ? meta_of(v.p.w) : 0u;
+      return __all_sync(0xffffffffu, (m & (M_FILLED | M_FIXED | kXY)) == (M_FILLED | kXY));
+    };
 #ifdef VX_RACE_OLDPARITY   // the round-1 parity (restarts per plane): the probe must catch it
-      const int par = (j - j0) & 1;
+#define VX_PAR(j) (((j) - j0) & 1)
 #else
-      const int par = rc & 1;
+#define VX_PAR(j) (rc & 1)
 #endif
-      if (full) row(std::true_type{}, j, va, vb, par);
-      else row(std::false_type{}, j, va, vb, par);
-      ++rc;
+    for (int j = j0; j < j1;) {
+      if (is_full(va)) {
+#ifdef VX_ROW_PAIRS
+        // two FULL rows per trip with the row registers' roles swapped: no copy
+        row(std::true_type{}, j, va, vb, VX_PAR(j));
+        ++rc;
+        ++j;
+        if (j < j1 && is_full(vb)) {
+          row(std::true_type{}, j, vb, va, VX_PAR(j));
+          ++rc;
+          ++j;
+          continue;
+        }
+#else
+        row(std::true_type{}, j, va, vb, VX_PAR(j));
+        ++rc;
+        ++j;
+#endif
+      } else {
+        row(std::false_type{}, j, va, vb, VX_PAR(j));
+        ++rc;
+        ++j;
+      }
       va = vb;
     }
+#undef VX_PAR
   }
   if constexpr (COLLIDE) budget_max(d, vmax);
 }
