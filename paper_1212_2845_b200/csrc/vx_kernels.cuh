@@ -1005,22 +1005,9 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_step_fused(Dev<
 #endif
     for (int j = j0; j < j1;) {
       if (is_full(va)) {
-#ifdef VX_ROW_PAIRS
-        // two FULL rows per trip with the row registers' roles swapped: no copy
         row(std::true_type{}, j, va, vb, VX_PAR(j));
         ++rc;
         ++j;
-        if (j < j1 && is_full(vb)) {
-          row(std::true_type{}, j, vb, va, VX_PAR(j));
-          ++rc;
-          ++j;
-          continue;
-        }
-#else
-        row(std::true_type{}, j, va, vb, VX_PAR(j));
-        ++rc;
-        ++j;
-#endif
       } else {
         row(std::false_type{}, j, va, vb, VX_PAR(j));
         ++rc;
