@@ -253,7 +253,16 @@ def run_ours(args):
         return 2
     torch.cuda.set_device(local)
     nid = None
-    if world > 1:
+    # --nccl-one: the x-slab rank path (NCCL communicator, ghost exchange, owned
+    # I/O, reductions over the group) with a single rank under torchrun --
+    # a check of the N > 1 code on one GPU (VX_FORCE_NCCL)
+    if args.nccl_one:
+        if world != 1 or "RANK" not in os.environ:
+            print("--nccl-one needs torchrun with one process", file=sys.stderr)
+            return 2
+        os.environ["VX_FORCE_NCCL"] = "1"
+    use_dist = world > 1 or args.nccl_one
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         nid = vd.bootstrap_nccl_id(dist, rank)
 
@@ -268,7 +277,7 @@ def run_ours(args):
     else:
         # C5 shards into x-slabs; C1-C4 are too small to shard and run as one
         # replica per GPU
-        shard = world > 1 and not replicas
+        shard = (world > 1 and not replicas) or args.nccl_one
         lat = from_scene(sc, precision=args.precision, device=local, rank=rank if shard else 0,
                          nranks=world if shard else 1, nccl_id=nid if shard else None,
                          init_state=sc.v0 is not None, engine=args.engine)
@@ -278,7 +287,7 @@ def run_ours(args):
 
     def barrier():
         torch.cuda.synchronize()
-        if world > 1:
+        if use_dist:
             dist.barrier(device_ids=[local])
 
     # warm-up (graphs captured / tables uploaded)
@@ -304,7 +313,7 @@ def run_ours(args):
         lat.step(args.steps)
         ev1.record(stream)
         barrier()
-        region_ms.append(vd.max_over_ranks([ev0.elapsed_time(ev1)], dist if world > 1 else None,
+        region_ms.append(vd.max_over_ranks([ev0.elapsed_time(ev1)], dist if use_dist else None,
                                            "cuda")[0])
     clocks = sampler.stop()
     ms_max = float(np.median(region_ms))
@@ -319,12 +328,12 @@ def run_ours(args):
     lat.step(args.steps)
     ie1.record(stream)
     barrier()
-    instr_ms = vd.max_over_ranks([ie0.elapsed_time(ie1)], dist if world > 1 else None, "cuda")[0]
+    instr_ms = vd.max_over_ranks([ie0.elapsed_time(ie1)], dist if use_dist else None, "cuda")[0]
     kt = lat.kernel_times()
     n_instr = max(1, round(kt["all"][1] / max(lat.launches_per_step, 1)))   # measured steps
     lat.set_instrumentation(False)
     per_rank = None
-    if world > 1:   # each rank's own kernel breakdown (ms per step), gathered on rank 0
+    if use_dist:   # each rank's own kernel breakdown (ms per step), gathered on rank 0
         mine = [kt[k][0] / n_instr for k in ("bonds", "integrate", "other", "all")]
         per_rank = vd.gather_rows(mine, dist, "cuda")
 
@@ -381,7 +390,7 @@ def run_ours(args):
                (st_init.pos, st_init.quat, st_init.linmom, st_init.angmom, st_init.latch))
         # x-slab ranks move only their own voxels (vx_set/read_state_owned); one
         # GPU or replicas use the full-state calls
-        owned = world > 1 and not replicas
+        owned = (world > 1 and not replicas) or args.nccl_one
         ids = lat.owned_ids() if owned else None
         if owned:
             st0 = tuple(a[ids] for a in st0)
@@ -407,11 +416,11 @@ def run_ours(args):
         tw = time.perf_counter() - tw
         ems = e0.elapsed_time(e1)
         # host wall clock around the calls bounds the device timeline
-        ems = max(vd.max_over_ranks([ems, tw * 1e3], dist if world > 1 else None, "cuda"))
+        ems = max(vd.max_over_ranks([ems, tw * 1e3], dist if use_dist else None, "cuda"))
         bi = sum(a.nbytes for a in hin)
         bo = sum(a.nbytes for a in (hout.pos, hout.quat, hout.linmom, hout.angmom, hout.latch))
-        bi = vd.max_over_ranks([bi], dist if world > 1 else None, "cuda")[0] if owned else bi
-        bo = vd.max_over_ranks([bo], dist if world > 1 else None, "cuda")[0] if owned else bo
+        bi = vd.max_over_ranks([bi], dist if use_dist else None, "cuda")[0] if owned else bi
+        bo = vd.max_over_ranks([bo], dist if use_dist else None, "cuda")[0] if owned else bo
         e2e = {"value": N * K / (ems / 1e3) * (world if replicas else 1), "unit": UNIT,
                "h2d_bytes_per_step": bi / K, "d2h_bytes_per_step": bo / K,
                "episode": f"set_state (H2D) + {K} steps + read_state (D2H) per episode; "
@@ -466,7 +475,7 @@ def run_ours(args):
                                             "rows": per_rank}
         print(json.dumps(line), flush=True)
     lat.destroy()
-    if world > 1:
+    if use_dist:
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()
     return 0
@@ -489,6 +498,8 @@ def main():
                     help="with --batch: scenes per z column ('auto' or an integer; 1 = along x only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--nccl-one", action="store_true",
+                    help="(check) the x-slab rank path with one rank under torchrun")
     ap.add_argument("--e2e-steps", type=int, default=0,
                     help="steps per end-to-end episode (default: the workload's own run length)")
     ap.add_argument("--no-cpu", action="store_true")

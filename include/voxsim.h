@@ -59,7 +59,8 @@ typedef struct {
   int32_t rank, nranks;     /* slab decomposition along x (nranks >= 1, <= nx)         */
   const void* nccl_id;      /* 128-byte ncclUniqueId from vx_nccl_unique_id() on rank 0,
                                broadcast by the caller: one process per GPU, ghost planes
-                               by NCCL send/recv.  NULL with nranks > 1 (rank 0): the
+                               by NCCL send/recv.  One id serves one lattice (as with
+                               ncclCommInitRank): create a new id for every lattice.  NULL with nranks > 1 (rank 0): the
                                nranks slabs are emulated inside this one handle on one
                                device (ghost planes by device copies) -- the same slab
                                arithmetic, used to test bitwise slab invariance.        */

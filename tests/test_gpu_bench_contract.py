@@ -48,3 +48,25 @@ def test_bench_line_reference():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_x_slab_rank_path_one_rank():
+    """bench.py's N > 1 code (NCCL communicator, ghost exchange, owned-voxel
+    I/O, digest summed over the group, per-rank rows) run with one rank under
+    torchrun (--nccl-one): the final-state digest equals the plain run's."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    args = ["--config", "C4", "--steps", "10", "--warmup", "3", "--no-cpu", "--e2e-steps", "64"]
+    plain = _run(*args)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "1", "--master-addr", "127.0.0.1", "--master-port",
+                          str(port), os.path.join(ROOT, "bench.py"), "--nccl-one", *args],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.strip()][-1])
+    assert line["config"]["parallelism"] == "x-slab1" and "per_rank_ms_per_step" in line
+    assert "vx_set/read_state_owned" in line["e2e"]["episode"]
+    assert line["e2e"]["final_state_digest"] == plain["e2e"]["final_state_digest"]

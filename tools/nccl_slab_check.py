@@ -33,12 +33,12 @@ def main():
     world, rank, local = vd.env_ranks()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    nid = vd.bootstrap_nccl_id(dist, rank)
     sc = W.block(nx, ny, nz)
     st0 = W.strained(sc, seed=4, lift=False)
     out = {"world": world, "shape": [nx, ny, nz], "steps": steps}
     ok = True
     for prec in (32, 64):
+        nid = vd.bootstrap_nccl_id(dist, rank)      # an NCCL unique id serves one communicator
         lat = from_scene(sc, precision=prec, rank=rank, nranks=world, nccl_id=nid,
                          init_state=False, engine="fused")
         ids = lat.owned_ids()
