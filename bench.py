@@ -51,8 +51,8 @@ ALG_BYTES = {
 # binary measured offline (ncu replays each kernel ~40 times, so it cannot run
 # inside the bench); `source` names the profile, and they go stale with every
 # kernel change until the next profile.
-FUSED_COUNTS = {32: {"warp_inst": 891170510 / 33554432, "fp32_ops": 587.1, "flop": 891.4,
-                     "source": "profiles/r14_full.json (issue slots), r13 (FP32 op mix); "
+FUSED_COUNTS = {32: {"warp_inst": 883301546 / 33554432, "fp32_ops": 587.1, "flop": 891.4,
+                     "source": "profiles/r15_full.json (issue slots), r13 (FP32 op mix); "
                                "ncu --set full, C5 fp32"}}
 
 
