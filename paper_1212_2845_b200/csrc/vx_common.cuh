@@ -201,14 +201,10 @@ template <class R> __device__ __forceinline__ V3<R> mulT(const Rot<R>& r, V3<R> 
 // sm_100's FP32x2 path: FADD2 / FMUL2 / FFMA2 perform two fp32 operations per
 // instruction, each half rounded exactly like the scalar instruction.  A
 // broadcast scalar, a swapped pair and a negated half are operand modifiers,
-// so pairing (x, y) halves the issue slots of 2-vector work.  The pairs are
-// float2 values and the operations the compiler's own sm_100 intrinsics
-// (__ffma2_rn, __fmul2_rn, __fadd2_rn) can express them too; inline PTX was
-// suspected of costing register moves
-// ... in principle: ptxas sees through the PTX movs as well and the SASS is the
-// same (MOV counts 455 vs 476 statically), so the PTX form stays the default and
-// -DVX_F2_BUILTIN selects the intrinsics.
-#ifndef VX_F2_BUILTIN
+// so pairing (x, y) halves the issue slots of 2-vector work.  Pairs live in
+// 64-bit registers: the halves of a loaded float4 / float2 are pairs already.
+// (The compiler's float2 intrinsics __ffma2_rn / __fmul2_rn / __fadd2_rn give
+// the same SASS; profiles/r14_experiments.md.)
 typedef unsigned long long f2_t;
 __device__ __forceinline__ f2_t f2pk(float lo, float hi) {
   f2_t r;
@@ -245,17 +241,6 @@ __device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
-#else
-typedef float2 f2_t;
-__device__ __forceinline__ f2_t f2pk(float lo, float hi) { return make_float2(lo, hi); }
-__device__ __forceinline__ float f2lo(f2_t r) { return r.x; }
-__device__ __forceinline__ float f2hi(f2_t r) { return r.y; }
-__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) { return __fadd2_rn(a, b); }
-// a - b = a + (-b): negation is exact, so this rounds like sub.rn.f32x2
-__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
-__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) { return __ffma2_rn(a, b, c); }
-#endif
 __device__ __forceinline__ f2_t bc2(float s) { return f2pk(s, s); }
 __device__ __forceinline__ f2_t zero2() { return f2pk(0.f, 0.f); }
 
