@@ -161,3 +161,23 @@ def test_shortlist_covers_every_overlap_each_step(prec):
         assert not missing, missing[:5]
     assert lat.num_rebuilds >= 2
     assert seen_overlap > 0
+
+
+@pytest.mark.parametrize("engine", ["fused", "two_pass"])
+@pytest.mark.parametrize("prec", [32, 64])
+def test_quaternion_sign_invariance(prec, engine):
+    """q and -q are one orientation (R7): negating every voxel's quaternion of a
+    strained block leaves positions and momenta bit for bit unchanged over 60
+    steps (the bond's w >= 0 fold, R(q) = R(-q)); the quaternions stay negated."""
+    sc = W.block(10, 9, 70, precision=prec)
+    pos, quat, P, phi, latch = W.strained(sc, seed=9, lift=False)
+    out = []
+    for sgn in (1.0, -1.0):
+        lat = from_scene(sc, precision=prec, engine=engine, init_state=False)
+        lat.set_state(pos, sgn * quat, P, phi, latch)
+        lat.step(60)
+        out.append(lat.read_state())
+    a, b = out
+    assert np.array_equal(a.pos, b.pos) and np.array_equal(a.linmom, b.linmom)
+    assert np.array_equal(a.angmom, b.angmom) and np.array_equal(a.latch, b.latch)
+    assert np.array_equal(a.quat, -b.quat)

@@ -340,3 +340,124 @@ def test_thermal_two_material_pair_rest_length_is_mean_alpha():
     sep = np.linalg.norm(st.pos[1] - st.pos[0])
     assert sep == pytest.approx(L * (1 + 0.5 * (aa + ab) * dT), rel=1e-9)
     assert np.abs(st.linmom).max() <= 1e-15
+
+
+# --------------------------------------------------------------- friction branches (R15)
+def _floor_voxel_state(o, m, pen, P=(0.0, 0.0, 0.0), latch=0):
+    o.set_state(np.array([[0.0, 0.0, 0.5 * L - pen]]), np.array([[1.0, 0, 0, 0]]),
+                np.array([list(P)]), np.zeros((1, 3)), np.array([latch], np.uint8))
+
+
+def test_friction_breakaway_first_step():
+    """A latched voxel pressed into the floor (F_n = k_f p) under a lateral force
+    beyond mu_s F_n breaks away (Eq. 36 violated) and feels F_l - mu_d F_n F_l/|F_l|
+    (Eq. 37, R15: opposite the applied force while V_l = 0), unlatched."""
+    E, rho, p, mus, mud = 1e6, 1000.0, 2e-6, 0.6, 0.3
+    o, s = sim(np.ones((1, 1, 1)), [mat(E=E, rho=rho, mu_s=mus, mu_d=mud)], floor_on=1)
+    m = rho * L ** 3
+    Fn = E * L * p
+    Fl = np.array([0.6, -0.8]) * (1.5 * mus * Fn)          # |F_l| = 1.5 mu_s F_n
+    o.set_boundary(None, np.array([[Fl[0], Fl[1], 0.0]]))
+    _floor_voxel_state(o, m, p, latch=1)
+    o.step(1)
+    st = o.read_state()
+    want = o.dt * (Fl - mud * Fn * Fl / np.linalg.norm(Fl))
+    assert st.latch[0] == 0
+    assert st.linmom[0, :2] == pytest.approx(want, rel=1e-12)
+    # just below the threshold it stays latched and does not move laterally
+    o2, _ = sim(np.ones((1, 1, 1)), [mat(E=E, rho=rho, mu_s=mus, mu_d=mud)], floor_on=1)
+    o2.set_boundary(None, np.array([[0.99 * mus * Fn, 0.0, 0.0]]))
+    _floor_voxel_state(o2, m, p, latch=1)
+    o2.step(1)
+    st2 = o2.read_state()
+    assert st2.latch[0] == 1 and st2.linmom[0, 0] == 0.0 and st2.pos[0, 0] == 0.0
+
+
+def test_latch_cleared_off_the_floor():
+    """Out of floor contact (p <= 0) the static-friction latch is released (R15)."""
+    o, s = sim(np.ones((1, 1, 1)), [mat(mu_s=0.5, mu_d=0.5)], floor_on=1)
+    _floor_voxel_state(o, 1e-6, -1e-6, latch=1)             # 1 um above the floor
+    o.step(1)
+    assert o.read_state().latch[0] == 0
+
+
+# --------------------------------------------------------------- thermal radii (R14, R16)
+def test_floor_radius_swells_with_temperature():
+    """A voxel resting exactly on the floor at its rest radius l/2 penetrates by
+    (l/2) alpha dT once the temperature rises (contact radius of R14); with no
+    gravity its first step gets P_z = dt k_f (l/2) alpha dT."""
+    E, rho, a, dT = 1e6, 1000.0, 0.01, 5.0
+    o, s = sim(np.ones((1, 1, 1)), [mat(E=E, rho=rho, cte=a)], floor_on=1, T_amp=dT,
+               T_freq=0.0, T_phase=math.pi / 2)
+    _floor_voxel_state(o, rho * L ** 3, 0.0)
+    o.step(1)
+    assert o.read_state().linmom[0, 2] == pytest.approx(o.dt * E * L * 0.5 * L * a * dT, rel=1e-12)
+
+
+def test_contact_radius_swells_with_temperature():
+    """Two voxels 1.01 l apart (no contact at rest radii) touch once dT swells
+    their radii to (l/2)(1 + alpha dT): force k_c (r_a + r_b - d) (R16)."""
+    aa, ab, dT = 0.02, 0.04, 1.0
+    cells = np.zeros((1, 1, 6), np.uint8)
+    cells[0, 0, 0] = 1
+    cells[0, 0, 5] = 2
+    o, s = sim(cells, [mat(cte=aa), mat(E=2e6, cte=ab)], self_collision=1, zeta_col=0.0,
+               T_amp=dT, T_freq=0.0, T_phase=math.pi / 2)
+    pos, quat, P, phi, latch = s.initial_state()
+    d = 1.01 * L
+    pos[1] = pos[0] + np.array([d, 0.0, 0.0])
+    o.set_state(pos, quat, P, phi, latch)
+    o.step(1)
+    kc = harmonic(1e6 * L, 2e6 * L)
+    q = 0.5 * L * (1 + aa * dT) + 0.5 * L * (1 + ab * dT) - d
+    assert q > 0
+    assert o.read_state().linmom[0, 0] == pytest.approx(-o.dt * kc * q, rel=1e-12)
+
+
+# --------------------------------------------------------------- R7, R16 invariants
+def test_bond_loads_invariant_under_quaternion_sign():
+    """q and -q are the same orientation: flipping the sign of voxel b's (or a's)
+    quaternion leaves every bond load unchanged (R7: the w >= 0 branch of the
+    rotation vector of q_a* q_b)."""
+    o, s = sim(np.array([[[1, 2]]]), [mat(), mat(E=3e6, rho=1500.0)], zeta_bond=0.7)
+    rng = np.random.default_rng(21)
+    for axis in range(3):
+        qa = Rotation.from_rotvec(rng.normal(size=3) * 0.3)
+        qb = Rotation.from_rotvec(qa.as_rotvec() + rng.normal(size=3) * 0.05)
+        def state(q, D, P, phi):
+            x, y, z, w = q.as_quat()
+            return np.r_[D, w, x, y, z, P, phi]
+        Da = np.zeros(3); Db = qa.apply(np.eye(3)[axis]) * L + rng.normal(size=3) * 1e-5
+        sa = state(qa, Da, rng.normal(size=3) * 1e-9, rng.normal(size=3) * 1e-14)
+        sb = state(qb, Db, rng.normal(size=3) * 1e-9, rng.normal(size=3) * 1e-14)
+        ref = np.concatenate(o.bond_loads(0, 1, axis, sa, sb))
+        for flip_a, flip_b in ((False, True), (True, False), (True, True)):
+            a2, b2 = sa.copy(), sb.copy()
+            if flip_a:
+                a2[3:7] *= -1
+            if flip_b:
+                b2[3:7] *= -1
+            got = np.concatenate(o.bond_loads(0, 1, axis, a2, b2))
+            assert got == pytest.approx(ref, rel=1e-12, abs=1e-12 * np.abs(ref).max())
+
+
+def test_interior_voxels_feel_no_contact():
+    """Self collision is between surface voxels: a foreign voxel placed on
+    the interior voxel of a 3x3x3 cube pushes on nothing (the centre is not a
+    surface voxel, and the intruder's partners are surface voxels only), so the
+    step equals the one without self collision for the cube's centre."""
+    cells = np.zeros((3, 3, 8), np.uint8)
+    cells[:, :, :3] = 1
+    cells[1, 1, 7] = 1
+    runs = []
+    for col in (0, 1):
+        o, s = sim(cells, [mat()], self_collision=col, zeta_col=0.0)
+        pos, quat, P, phi, latch = s.initial_state()
+        ijk = s.voxel_coords()
+        centre = int(np.nonzero((ijk == [1, 1, 1]).all(1))[0][0])
+        intruder = int(np.nonzero((ijk == [7, 1, 1]).all(1))[0][0])
+        pos[intruder] = pos[centre] + np.array([0.3 * L, 0.0, 0.0])
+        o.set_state(pos, quat, P, phi, latch)
+        o.step(1)
+        runs.append(o.read_state().linmom[centre])
+    assert np.array_equal(runs[0], runs[1])

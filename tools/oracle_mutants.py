@@ -92,6 +92,28 @@ MUTANTS = [
      "double J = l * l * l * l / 6.0;", "double J = l * l * l * l / 12.0;"),
     ("contact Manhattan exclusion <= 2", "P:280",
      "if (manhattan(vx, s->vox[p]) <= 3) continue;", "if (manhattan(vx, s->vox[p]) <= 2) continue;"),
+    ("breakaway friction along +F_l", "Eq. 37, R15",
+     "F.x = Flx - M.mu_d * Fn * Flx / Fl;", "F.x = Flx + M.mu_d * Fn * Flx / Fl;"),
+    ("breakaway with mu_s", "Eq. 37, R15",
+     "F.y = Fly - M.mu_d * Fn * Fly / Fl;", "F.y = Fly - M.mu_s * Fn * Fly / Fl;"),
+    ("sliding friction without the F_n factor", "Eq. 37",
+     "F.x = Flx - M.mu_d * Fn * V.x / Vl;", "F.x = Flx - M.mu_d * V.x / Vl;"),
+    ("latch kept when leaving the floor", "R15",
+     "      } else {\n        latch = false;\n      }\n    }\n    /* Eq. 27-30 (R6) */", "      }\n    }\n    /* Eq. 27-30 (R6) */"),
+    ("ground damping on velocity of the wrong sign", "P:254",
+     "F = F - cgt * V;", "F = F + cgt * V;"),
+    ("thermal floor radius without alpha", "R14",
+     "double rv = 0.5 * l * (1.0 + M.cte * dT);", "double rv = 0.5 * l;"),
+    ("contact radius without thermal swell", "R16",
+     "double ra = 0.5 * s->l * (1.0 + ma.cte * dT);\n  double rb", "double ra = 0.5 * s->l;\n  double rb"),
+    ("rotation vector without the factor 2", "R7",
+     "th = (2.0 * std::atan2(vn, qrel.w) / vn) * vq;", "th = (std::atan2(vn, qrel.w) / vn) * vq;"),
+    ("no w >= 0 fold of q_rel", "R7",
+     "if (qrel.w < 0) { qrel.w = -qrel.w; qrel.x = -qrel.x; qrel.y = -qrel.y; qrel.z = -qrel.z; }", ""),
+    ("contact for interior voxels too", "P:278",
+     "if (env.self_collision && vx.surface) {", "if (env.self_collision) {"),
+    ("temperature phase dropped", "P:293",
+     "std::sin(2 * kPi * s->env.T_freq * t + s->env.T_phase)", "std::sin(2 * kPi * s->env.T_freq * t)"),
 ]
 
 
