@@ -2,12 +2,12 @@
 #   bash tools/ab_ncu_geo.sh lib.so:4:16 lib2.so:4:-1 ...   (SX < 0: ranged split, -SX waves)
 mkdir -p gpurun_out
 cp paper_1212_2845_b200/libvoxsim.so /tmp/lib_orig.so
-for pass in 1 2; do
+for pass in ${PASSES:-1 2}; do
   for spec in "$@"; do
     IFS=: read lib ty sx <<< "$spec"
     cp $lib paper_1212_2845_b200/libvoxsim.so
     VX_FUSED_TY=$ty VX_FUSED_SX=$sx timeout 600 ncu --metrics gpu__time_duration.sum --clock-control base \
-      -k regex:k_step_fused -s 20 -c 15 --csv python tools/ab_time.py x > /tmp/ab_ncu.csv 2>/dev/null
+      -k regex:k_step_fused -s 20 -c ${NCNT:-15} --csv python tools/ab_time.py x > /tmp/ab_ncu.csv 2>/dev/null
     python - "$spec" <<'PY'
 import csv, sys, statistics
 rows = [r for r in csv.reader(open("/tmp/ab_ncu.csv")) if len(r) > 10]
